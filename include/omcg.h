@@ -1,0 +1,170 @@
+/*
+ * omcg.h — C ABI of the B200-native event-based Monte Carlo transport hot path
+ * (libomcg.so). This is the "thin C-ABI layer" between the C++ host driver and
+ * the sm_100a kernels named by BASELINE.json's north_star.
+ *
+ * What each entry point replaces in the reference (arxiv/paper_2402_09222,
+ * /root/reference/proj):
+ *   - The reference reaches the transport loop only through a process boundary:
+ *     `openmc --event -i #P1 -b #P2 -m #P3` / `openmc-queueless --event -i #P1
+ *     -b #P2` (campaigns/openmc/openmc.sh.in:5,7), FoM parsed from stdout with
+ *     `FOM:\s*([0-9.eE+-]+)\s*particles/s` (campaigns/openmc/campaign.json:8,
+ *     last match wins, src/harness.cpp:150-171), energy from metrics.txt
+ *     (src/harness.cpp:117-136). omcg_run() is that binary's body: the
+ *     `openmc` executable built from this repo (tools: bin/openmc) is a thin
+ *     argv/env front end over it.
+ *   - omcg_run_config mirrors the seven tuned parameters P0..P6
+ *     (campaigns/openmc/space.json:3-9; Table 1).
+ *   - Conventions follow the reference C ABI (include/autotune/autotune.h:13-41,
+ *     src/capi.cpp:24-76): int return codes, no exception crosses the ABI,
+ *     thread-local omcg_last_error(), opaque handles, only these symbols exported.
+ *   - An in-process evaluator (the reference's Evaluator plugin type,
+ *     src/harness.hpp:102) would call omcg_run() directly; see INTEGRATION.md.
+ */
+#ifndef OMCG_H
+#define OMCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(OMCG_BUILDING)
+#define OMCG_API __attribute__((visibility("default")))
+#else
+#define OMCG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    OMCG_OK = 0,
+    OMCG_EINVAL = 1, /* invalid argument / configuration */
+    OMCG_EIO = 2,    /* filesystem failure */
+    OMCG_ECUDA = 3,  /* CUDA runtime / driver failure (no device, OOM, ...) */
+    OMCG_ENCCL = 4,  /* NCCL failure */
+    OMCG_EFAIL = 5   /* unexpected internal failure */
+};
+
+enum { OMCG_PINCELL = 0, OMCG_ASSEMBLY = 1, OMCG_CORE = 2 };
+enum { OMCG_QUEUED = 0, OMCG_QUEUELESS = 1 };           /* P0 */
+enum { OMCG_BIND_CORES = 0, OMCG_BIND_THREADS = 1, OMCG_BIND_SOCKETS = 2 }; /* P6 */
+enum { OMCG_N_SCORES = 4 };   /* per pin: flux, absorption, fission, nu-fission */
+enum { OMCG_MAX_BATCHES = 512 };
+
+typedef struct omcg_problem omcg_problem;
+
+typedef struct {
+    int kind;
+    int n_nuclides;
+    int n_materials;
+    int nx, ny;
+    int n_tally_bins;      /* nx*ny pins; OMCG_N_SCORES scores each */
+    int fuel_nuclides;
+    int64_t n_grid_total;
+    int64_t lib_bytes;     /* E + 4-channel rows, bytes */
+    double gen_seconds;    /* host library generation time */
+} omcg_problem_info;
+
+typedef struct {
+    /* tuned parameters (campaigns/openmc/space.json) */
+    int mode;                     /* P0: OMCG_QUEUED ("openmc") or OMCG_QUEUELESS */
+    int64_t particles_in_flight;  /* P1 (-i): in-flight bank slots per task */
+    int n_bins;                   /* P2 (-b): log hash-grid bins */
+    int64_t sort_threshold;       /* P3 (-m): sort fuel XS queue when len >= P3; <0 never */
+    int host_threads;             /* P4 (-c): host threads for initialisation */
+    int tasks_per_gpu;            /* P5 (--ntasks-per-gpu): concurrent sub-banks per GPU */
+    int cpu_bind;                 /* P6 (--cpu-bind) */
+    /* problem size */
+    int64_t n_particles;          /* histories per batch (whole job) */
+    int n_batches;
+    int n_inactive;
+    uint64_t seed;                /* transport master seed */
+    /* placement: either n_gpus devices in this process (devices[] or 0..n-1),
+     * or one rank of a multi-process job (world_size > 1, nccl_id set). */
+    int n_gpus;
+    int devices[8];
+    int world_size;
+    int rank;
+    unsigned char nccl_id[128];
+    /* diagnostics */
+    int record_batch;             /* 1-based batch whose first record_n histories are recorded */
+    int64_t record_n;
+    int profile;                  /* time every kernel class with CUDA events */
+    int trace_queues;             /* record per-iteration (queue, length, id-checksum) */
+} omcg_run_config;
+
+typedef struct {
+    int32_t n_xs, n_adv, n_cross, n_coll, n_sites, term;
+    double e_final, x_final;
+} omcg_record;
+
+typedef struct {
+    int n_batches_run;
+    double k_coll[OMCG_MAX_BATCHES];
+    double k_abs[OMCG_MAX_BATCHES];
+    double k_track[OMCG_MAX_BATCHES];
+    int64_t n_sites[OMCG_MAX_BATCHES];
+    int64_t n_events[4];          /* xs, advance, cross, collision */
+    int64_t n_leaked, n_absorbed, n_lost;
+    double k_mean, k_std;
+    double t_init;                /* upload + hash build + allocation, s */
+    double t_active;              /* active batches, s (device-event timed, max over ranks) */
+    double t_total;               /* all batches, s */
+    double fom;                   /* n_particles * n_active / t_active */
+    double energy_j;              /* NVML GPU energy over the call, J (0 if unavailable) */
+    int64_t kernel_launches;      /* launches inside the active batches */
+    int64_t kernel_launches_total;
+    int64_t h2d_bytes, d2h_bytes; /* host<->device traffic of the call */
+    /* profile (profile != 0): per kernel class, active batches */
+    double prof_ms[8];            /* xs_fuel, xs_nonfuel, advance, cross, collision, sort, compact, other */
+    int64_t prof_launches[8];
+    int64_t prof_items[8];        /* queue entries processed */
+    double xs_fuel_bytes;         /* algorithmic bytes of the fuel XS launches */
+    int64_t queue_iterations;     /* host event-loop iterations, all batches */
+    int64_t sorts;                /* fuel-queue sorts performed */
+} omcg_run_result;
+
+OMCG_API const char* omcg_version(void);
+OMCG_API const char* omcg_last_error(void);
+
+/* ---- problem (host buffers) ---- */
+OMCG_API int omcg_problem_create(int kind, uint64_t xs_seed, int host_threads, omcg_problem** out);
+OMCG_API void omcg_problem_free(omcg_problem* p);
+OMCG_API int omcg_problem_get_info(const omcg_problem* p, omcg_problem_info* info);
+OMCG_API uint64_t omcg_library_checksum(const omcg_problem* p);
+
+/* ---- device-side building blocks (parity hooks) ---- */
+/* Build the log hash grid for n_bins on `device` and return its FNV-1a checksum
+ * (same definition as the oracle's orc_hash_checksum); optionally copy it out
+ * (n_nuclides*(n_bins+1) int32, nuclide-major). */
+OMCG_API int omcg_hash_build(const omcg_problem* p, int n_bins, int device, uint64_t* checksum,
+                             int32_t* hash_out);
+/* Macroscopic XS for n (material, E) pairs through the calculate_xs kernel:
+ * out = 4n doubles (total, absorption, fission, nu-fission). */
+OMCG_API int omcg_xs_lookup(const omcg_problem* p, int n_bins, int device, int64_t n,
+                            const int32_t* mat, const double* E, double* out);
+
+/* ---- the transport run (the `openmc --event` body) ---- */
+OMCG_API void omcg_run_config_default(omcg_run_config* cfg);
+OMCG_API int omcg_run(const omcg_problem* p, const omcg_run_config* cfg, omcg_run_result* res,
+                      int64_t* tally_out, omcg_record* records);
+/* Per-iteration queue trace of the last omcg_run with trace_queues != 0:
+ * triples (queue id, length, checksum of particle ids). */
+OMCG_API int64_t omcg_queue_trace(int64_t* out, int64_t max_entries);
+
+/* NCCL unique id for a multi-process job (rank 0 creates, others receive). */
+OMCG_API int omcg_nccl_unique_id(unsigned char out[128]);
+OMCG_API int omcg_device_count(int* n);
+
+/* Host-side fission-bank redistribution plan used between batches of a
+ * multi-GPU run. S_all: canonical bank size of every rank;
+ * off: the batch's resampling offset. plan (4*world+2 int64): send_first[w],
+ * send_count[w], recv_first[w], recv_count[w], need_first, need_count. */
+OMCG_API int omcg_bank_exchange_plan(const uint64_t* S_all, int world, int64_t n_batch, uint64_t off, int rank,
+                                     int64_t* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OMCG_H */

@@ -1,0 +1,63 @@
+// device.cuh — device-side data layout of the transport hot path.
+//
+// HBM layout (per GPU):
+//   library  : E[]  f64, all nuclide grids concatenated (goff[] offsets)
+//              xs[] XS4 (32 B rows: total, absorption, fission, nu-fission)
+//   hash     : int32 [n_nuc][n_bins+1], nuclide-major (P2 bins)
+//   bank     : structure-of-arrays over P1 in-flight slots
+//   queues   : int32 slot lists, one per event type, rebuilt in slot order
+//   fission  : unordered append buffer of 40 B sites + per-history counts,
+//              canonicalised to (history, progeny) order at batch end.
+#pragma once
+#include <cstdint>
+
+#include "../../include/omcg.h"
+#include "omcg_physics.cuh"
+#include "problem.hpp"
+
+namespace omcg {
+
+struct DevLib {
+    int n_nuc, n_bins, n_mat;
+    double inv_spacing, log_emin;
+    const int32_t* goff;     // n_nuc+1
+    const double* E;
+    const XS4* xs;
+    const int32_t* hash;     // n_nuc*(n_bins+1)
+    const double* awr;       // n_nuc
+    const int32_t* mat_off;  // n_mat+1
+    const int32_t* mat_nuc;
+    const double* mat_dens;
+    const uint8_t* mat_fissionable;
+    const uint8_t* mat_fuel;  // material uses the fuel XS queue
+    const uint8_t* mat_sort_rank;  // fuel material rank for the sort key
+};
+
+struct Site {
+    double x, y, z, E;
+    uint64_t key;  // (batch-global history index << 24) | progeny
+};
+
+struct Bank {
+    int64_t cap;
+    double *x, *y, *z, *u, *v, *w, *E, *wgt;
+    double *st, *sa, *sf, *snf;
+    uint64_t* seed;
+    int32_t *gidx, *cell;
+    int8_t *ring, *mat, *surf, *event;
+    int32_t *n_xs, *n_adv, *n_cross, *n_coll, *n_sites;
+};
+
+// Per-rank accumulators shared by the rank's sub-banks (tasks).
+struct Acc {
+    unsigned long long* tally;   // n_tally_bins * 4 (fixed point)
+    unsigned long long* k;       // [0] collision, [1] absorption, [2] track length
+    unsigned long long* counts;  // [0..3] events xs/adv/cross/coll, [4+term] absorbed/leaked/lost
+    Site* bank;                  // unordered fission sites
+    unsigned long long* bank_count;
+    int64_t bank_cap;
+    int32_t* sites_pp;           // per rank-local history: sites banked
+    omcg_record* records;        // nullptr unless recording
+};
+
+}  // namespace omcg

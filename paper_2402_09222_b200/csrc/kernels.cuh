@@ -1,0 +1,68 @@
+// kernels.cuh — launch interface of the sm_100a event kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace omcg {
+
+// Everything an event kernel needs, passed by value as the kernel parameter.
+struct Ctx {
+    DevLib lib;
+    Geometry geo;  // geo.pin_map is a device pointer
+    Bank b;
+    Acc acc;
+    int tally_on;
+    int n_tally_bins;
+    int tally_smem;       // 1: aggregate tallies in shared memory (few bins)
+    double k_norm;
+    int64_t rank_lo;      // batch-global index of this rank's first history
+    int64_t n_batch;      // histories per batch, whole job
+    int batch;            // 1-based
+    uint64_t master;
+    int64_t record_n;
+    int recording;
+    unsigned long long* ctrl;  // [0] refill ticket, [1] alive, [2] error flags
+};
+
+struct Queues {
+    int32_t* q[N_QUEUES];
+};
+
+constexpr int SMEM_TALLY_MAX = 2048;  // tally bins*scores aggregated per block in smem
+
+// bookkeeping
+void reset_launch_counter();
+long long launch_counter();
+
+// library / hash
+void launch_hash_build(const DevLib& lib, int32_t* hash, cudaStream_t s);
+void launch_xs_pairs(const DevLib& lib, int64_t n, const int32_t* mat, const double* E, double* out,
+                     cudaStream_t s);
+
+// queue compaction (deterministic, slot order)
+void launch_compact(const int8_t* event, int64_t cap, int32_t* block_counts, int nb, unsigned int* totals,
+                    Queues qs, const int32_t* gidx, unsigned long long* trace_chk, cudaStream_t s);
+
+// event kernels; q == nullptr selects the queueless variant over all cap slots
+void launch_init(const Ctx& c, const int32_t* dead_q, int n, int64_t first_local, const Site* src,
+                 cudaStream_t s);
+void launch_refill_all(const Ctx& c, int64_t first_local, int64_t n_remaining, const Site* src,
+                       cudaStream_t s);
+void launch_xs(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
+void launch_advance(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
+void launch_cross(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
+void launch_collide(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
+
+// material/energy sort of the fuel XS queue (16-bit energy radix per material)
+void launch_sort(const Ctx& c, const int32_t* q_in, int32_t* q_out, int n, int n_fuel_mats,
+                 unsigned int* hist, unsigned int* cursor, uint32_t* keys, cudaStream_t s);
+
+// fission bank: canonical order + systematic resampling
+void launch_scan_i32(const int32_t* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);
+void launch_bank_canon(const Site* bank, int64_t n_sites, const int64_t* offsets, int64_t rank_lo,
+                       Site* canon, cudaStream_t s);
+void launch_resample(const Site* src, int64_t src_first, uint64_t S, uint64_t off, int64_t n_batch,
+                     int64_t rank_lo, int64_t n_local, Site* out, cudaStream_t s);
+
+}  // namespace omcg

@@ -1,0 +1,858 @@
+// transport.cu — host driver of the event-based transport loop on B200.
+//
+// One host thread per GPU (rank) and, inside it, P5 sub-banks ("tasks per
+// GPU") each with its own CUDA stream, in-flight bank of P1
+// slots, queues and host thread. Queued mode (P0 = "openmc") reads the queue
+// lengths back after each compaction and launches the kernel of the longest
+// queue, sorting the fuel XS queue first when its length >= P3; queueless
+// mode (P0 = "openmc-queueless") sweeps all event kernels over every slot
+// (PAPER.md:219-221). Between batches the rank reduces int64 tallies and
+// k-eff accumulators with NCCL and redistributes the canonical fission bank.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <thread>
+
+#include "kernels.cuh"
+#include "transport.hpp"
+
+namespace omcg {
+
+#define CK(x)                                                                                      \
+    do {                                                                                           \
+        cudaError_t e_ = (x);                                                                      \
+        if (e_ != cudaSuccess)                                                                     \
+            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" + \
+                            std::to_string(__LINE__) + ")");                                       \
+    } while (0)
+#define NK(x)                                                                         \
+    do {                                                                              \
+        ncclResult_t r_ = (x);                                                        \
+        if (r_ != ncclSuccess) throw NcclError(std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+using ull = unsigned long long;
+
+namespace {
+
+std::mutex g_trace_mu;
+std::vector<int64_t> g_trace;
+
+// Device allocations owned by one object, freed on destruction.
+struct DevArena {
+    std::vector<void*> ptrs;
+    int device = 0;
+    template <typename T>
+    T* alloc(int64_t n) {
+        void* p = nullptr;
+        if (n <= 0) n = 1;
+        CK(cudaMalloc(&p, sizeof(T) * (size_t)n));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~DevArena() {
+        if (ptrs.empty()) return;
+        cudaSetDevice(device);
+        for (void* p : ptrs) cudaFree(p);
+    }
+};
+
+// Library + hash grid + geometry resident in one GPU's HBM.
+struct GpuProblem {
+    DevArena arena;
+    DevLib lib{};
+    Geometry geo{};
+    int n_fuel_mats = 0;
+    int64_t h2d_bytes = 0;
+
+    void upload(const Problem& p, int n_bins, int device, cudaStream_t s) {
+        arena.device = device;
+        if (n_bins < 1 || n_bins > 10000000) throw std::invalid_argument("n_bins (P2) out of range");
+        const int nn = p.n_nuc, nm = (int)p.mat.size();
+        std::vector<int32_t> goff(nn + 1);
+        for (int i = 0; i <= nn; ++i) goff[i] = (int32_t)p.goff[i];
+        std::vector<int32_t> moff(nm + 1), mnuc;
+        std::vector<double> mdens;
+        std::vector<uint8_t> mfis(nm), mfuel(nm), mrank(nm);
+        int fuel_rank = 0;
+        for (int m = 0; m < nm; ++m) {
+            moff[m] = (int32_t)mnuc.size();
+            for (size_t i = 0; i < p.mat[m].nuc.size(); ++i) {
+                mnuc.push_back(p.mat[m].nuc[i]);
+                mdens.push_back(p.mat[m].dens[i]);
+            }
+            mfis[m] = p.mat[m].fissionable;
+            mfuel[m] = p.mat[m].fissionable;  // fissionable materials use the fuel XS queue
+            mrank[m] = p.mat[m].fissionable ? (uint8_t)fuel_rank++ : 0;
+        }
+        moff[nm] = (int32_t)mnuc.size();
+        n_fuel_mats = std::max(1, fuel_rank);
+        auto up = [&](auto* dst, const auto* src, size_t n) {
+            size_t bytes = sizeof(*src) * n;
+            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+            h2d_bytes += (int64_t)bytes;
+        };
+        int32_t* d_goff = arena.alloc<int32_t>(nn + 1);
+        double* d_E = arena.alloc<double>(p.grid_points());
+        XS4* d_xs = arena.alloc<XS4>(p.grid_points());
+        double* d_awr = arena.alloc<double>(nn);
+        int32_t* d_moff = arena.alloc<int32_t>(nm + 1);
+        int32_t* d_mnuc = arena.alloc<int32_t>((int64_t)mnuc.size());
+        double* d_mdens = arena.alloc<double>((int64_t)mdens.size());
+        uint8_t* d_mfis = arena.alloc<uint8_t>(nm);
+        uint8_t* d_mfuel = arena.alloc<uint8_t>(nm);
+        uint8_t* d_mrank = arena.alloc<uint8_t>(nm);
+        uint8_t* d_pin = arena.alloc<uint8_t>((int64_t)p.pin_map_host.size());
+        int32_t* d_hash = arena.alloc<int32_t>((int64_t)(n_bins + 1) * nn);
+        up(d_goff, goff.data(), goff.size());
+        up(d_E, p.E.data(), p.E.size());
+        up(d_xs, p.xs.data(), p.xs.size());
+        up(d_awr, p.awr.data(), p.awr.size());
+        up(d_moff, moff.data(), moff.size());
+        up(d_mnuc, mnuc.data(), mnuc.size());
+        up(d_mdens, mdens.data(), mdens.size());
+        up(d_mfis, mfis.data(), mfis.size());
+        up(d_mfuel, mfuel.data(), mfuel.size());
+        up(d_mrank, mrank.data(), mrank.size());
+        up(d_pin, p.pin_map_host.data(), p.pin_map_host.size());
+        const double log_emin = det_log(E_MIN);
+        const double ln_range = det_log(E_MAX) - log_emin;
+        lib.n_nuc = nn;
+        lib.n_bins = n_bins;
+        lib.n_mat = nm;
+        lib.inv_spacing = (double)n_bins / ln_range;
+        lib.log_emin = log_emin;
+        lib.goff = d_goff; lib.E = d_E; lib.xs = d_xs; lib.hash = d_hash; lib.awr = d_awr;
+        lib.mat_off = d_moff; lib.mat_nuc = d_mnuc; lib.mat_dens = d_mdens;
+        lib.mat_fissionable = d_mfis; lib.mat_fuel = d_mfuel; lib.mat_sort_rank = d_mrank;
+        launch_hash_build(lib, d_hash, s);
+        CK(cudaGetLastError());
+        geo = p.geo;
+        geo.pin_map = d_pin;
+    }
+};
+
+struct SubBank {
+    cudaStream_t stream = nullptr;
+    Bank b{};
+    int32_t* q[N_QUEUES] = {};
+    int32_t* q_sorted = nullptr;
+    uint32_t* keys = nullptr;
+    unsigned* hist = nullptr;
+    unsigned* cursor = nullptr;
+    int32_t* block_counts = nullptr;
+    int nb = 0;
+    unsigned* d_totals = nullptr;
+    unsigned* h_totals = nullptr;  // pinned
+    ull* ctrl = nullptr;           // [0] ticket [1] alive [2] errors
+    ull* h_ctrl = nullptr;         // pinned
+    ull* trace_chk = nullptr;
+    ull* h_trace_chk = nullptr;
+    int64_t lo = 0, hi = 0;        // rank-local history range
+    std::vector<int64_t> trace;
+    // profile
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    double prof_ms[8] = {};
+    int64_t prof_launches[8] = {};
+    int64_t prof_items[8] = {};
+    double xs_fuel_bytes = 0.0;
+    int64_t iterations = 0, sorts = 0;
+};
+
+struct RankShared {
+    // collective results of all ranks (max over ranks etc.)
+    std::mutex mu;
+};
+
+struct Rank {
+    int device = 0, rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    DevArena arena;
+    GpuProblem gp;
+    Acc acc{};
+    int n_tally_bins = 0;
+    int64_t N = 0, N_rank = 0, rank_lo = 0, bank_cap = 0;
+    Site* source = nullptr;
+    Site* canon = nullptr;
+    Site* recv = nullptr;
+    int64_t* scan_out = nullptr;
+    int64_t* scan_tmp = nullptr;
+    ull* d_sall = nullptr;  // allgathered bank counts
+    double* d_time = nullptr;
+    cudaStream_t main = nullptr;
+    cudaEvent_t ev_a0 = nullptr, ev_a1 = nullptr;
+    std::vector<SubBank> subs;
+    std::vector<DevArena> sub_arenas;
+    // host results
+    std::vector<int64_t> tally_total;
+    double k_coll[OMCG_MAX_BATCHES] = {}, k_abs[OMCG_MAX_BATCHES] = {}, k_track[OMCG_MAX_BATCHES] = {};
+    int64_t n_sites[OMCG_MAX_BATCHES] = {};
+    int64_t counts[7] = {};
+    int batches_run = 0;
+    double t_active = 0.0, t_init = 0.0;
+    long long launches_active = 0;
+    int64_t h2d = 0, d2h = 0;
+    std::string error;
+};
+
+// ------------------------------------------------------------------ setup
+void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
+    auto t0 = std::chrono::steady_clock::now();
+    CK(cudaSetDevice(R.device));
+    R.arena.device = R.device;
+    CK(cudaStreamCreateWithFlags(&R.main, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&R.ev_a0));
+    CK(cudaEventCreate(&R.ev_a1));
+    R.gp.upload(p, cfg.n_bins, R.device, R.main);
+    R.h2d += R.gp.h2d_bytes;
+    R.N = cfg.n_particles;
+    R.rank_lo = R.N * R.rank / R.world;
+    R.N_rank = R.N * (R.rank + 1) / R.world - R.rank_lo;
+    R.n_tally_bins = p.geo.nx * p.geo.ny;
+    R.bank_cap = 3 * R.N_rank + 4096;
+    R.acc.tally = R.arena.alloc<ull>(4 * (int64_t)R.n_tally_bins);
+    R.acc.k = R.arena.alloc<ull>(3);
+    R.acc.counts = R.arena.alloc<ull>(8);
+    R.acc.bank = R.arena.alloc<Site>(R.bank_cap);
+    R.acc.bank_count = R.arena.alloc<ull>(1);
+    R.acc.bank_cap = R.bank_cap;
+    R.acc.sites_pp = R.arena.alloc<int32_t>(R.N_rank);
+    R.acc.records = nullptr;
+    if (cfg.record_batch > 0 && cfg.record_n > 0) R.acc.records = R.arena.alloc<omcg_record>(cfg.record_n);
+    R.source = R.arena.alloc<Site>(R.N_rank);
+    R.canon = R.arena.alloc<Site>(R.bank_cap);
+    if (R.world > 1) R.recv = R.arena.alloc<Site>(R.bank_cap + R.N_rank);
+    R.scan_out = R.arena.alloc<int64_t>(R.N_rank);
+    R.scan_tmp = R.arena.alloc<int64_t>((R.N_rank + 1023) / 1024 + 1);
+    R.d_sall = R.arena.alloc<ull>(R.world);
+    R.d_time = R.arena.alloc<double>(1);
+    R.tally_total.assign(4 * (size_t)R.n_tally_bins, 0);
+
+    const int tasks = std::max(1, cfg.tasks_per_gpu);
+    R.subs.resize(tasks);
+    R.sub_arenas.resize(tasks);
+    for (int t = 0; t < tasks; ++t) {
+        SubBank& S = R.subs[t];
+        DevArena& A = R.sub_arenas[t];
+        A.device = R.device;
+        S.lo = R.N_rank * t / tasks;
+        S.hi = R.N_rank * (t + 1) / tasks;
+        int64_t cap = std::min<int64_t>(std::max<int64_t>(cfg.particles_in_flight, 1), std::max<int64_t>(S.hi - S.lo, 1));
+        if (cap > (int64_t)1 << 30) throw std::invalid_argument("particles in flight too large");
+        S.b.cap = cap;
+        CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+        Bank& B = S.b;
+        B.x = A.alloc<double>(cap); B.y = A.alloc<double>(cap); B.z = A.alloc<double>(cap);
+        B.u = A.alloc<double>(cap); B.v = A.alloc<double>(cap); B.w = A.alloc<double>(cap);
+        B.E = A.alloc<double>(cap); B.wgt = A.alloc<double>(cap);
+        B.st = A.alloc<double>(cap); B.sa = A.alloc<double>(cap); B.sf = A.alloc<double>(cap);
+        B.snf = A.alloc<double>(cap);
+        B.seed = A.alloc<uint64_t>(cap);
+        B.gidx = A.alloc<int32_t>(cap); B.cell = A.alloc<int32_t>(cap);
+        B.ring = A.alloc<int8_t>(cap); B.mat = A.alloc<int8_t>(cap); B.surf = A.alloc<int8_t>(cap);
+        B.event = A.alloc<int8_t>(cap);
+        B.n_xs = A.alloc<int32_t>(cap); B.n_adv = A.alloc<int32_t>(cap); B.n_cross = A.alloc<int32_t>(cap);
+        B.n_coll = A.alloc<int32_t>(cap); B.n_sites = A.alloc<int32_t>(cap);
+        CK(cudaMemsetAsync(B.event, EV_DEAD, (size_t)cap, S.stream));
+        for (int k = 0; k < N_QUEUES; ++k) S.q[k] = A.alloc<int32_t>(cap);
+        S.q_sorted = A.alloc<int32_t>(cap);
+        S.keys = A.alloc<uint32_t>(cap);
+        S.hist = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
+        S.cursor = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
+        CK(cudaMemsetAsync(S.hist, 0, sizeof(unsigned) * (size_t)R.gp.n_fuel_mats * 65536, S.stream));
+        S.nb = (int)((cap + 1023) / 1024);
+        S.block_counts = A.alloc<int32_t>((int64_t)N_QUEUES * S.nb);
+        S.d_totals = A.alloc<unsigned>(N_QUEUES);
+        S.ctrl = A.alloc<ull>(4);
+        S.trace_chk = A.alloc<ull>(N_QUEUES);
+        CK(cudaMemsetAsync(S.ctrl, 0, sizeof(ull) * 4, S.stream));
+        CK(cudaMallocHost(&S.h_totals, sizeof(unsigned) * N_QUEUES));
+        CK(cudaMallocHost(&S.h_ctrl, sizeof(ull) * 4));
+        CK(cudaMallocHost(&S.h_trace_chk, sizeof(ull) * N_QUEUES));
+        CK(cudaEventCreate(&S.e0));
+        CK(cudaEventCreate(&S.e1));
+        CK(cudaStreamSynchronize(S.stream));
+    }
+    CK(cudaStreamSynchronize(R.main));
+    R.t_init = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void teardown_rank(Rank& R) {
+    cudaSetDevice(R.device);
+    for (auto& S : R.subs) {
+        if (S.stream) cudaStreamDestroy(S.stream);
+        if (S.h_totals) cudaFreeHost(S.h_totals);
+        if (S.h_ctrl) cudaFreeHost(S.h_ctrl);
+        if (S.h_trace_chk) cudaFreeHost(S.h_trace_chk);
+        if (S.e0) cudaEventDestroy(S.e0);
+        if (S.e1) cudaEventDestroy(S.e1);
+    }
+    if (R.main) cudaStreamDestroy(R.main);
+    if (R.ev_a0) cudaEventDestroy(R.ev_a0);
+    if (R.ev_a1) cudaEventDestroy(R.ev_a1);
+}
+
+// ------------------------------------------------------------------ event loops
+struct Prof {
+    SubBank& S;
+    bool on;
+    int cls;
+    int64_t items;
+    Prof(SubBank& s, bool enabled, int c, int64_t n) : S(s), on(enabled), cls(c), items(n) {
+        if (on) CK(cudaEventRecord(S.e0, S.stream));
+    }
+    ~Prof() {
+        if (!on) return;
+        float ms = 0.f;
+        if (cudaEventRecord(S.e1, S.stream) != cudaSuccess || cudaEventSynchronize(S.e1) != cudaSuccess ||
+            cudaEventElapsedTime(&ms, S.e0, S.e1) != cudaSuccess)
+            return;
+        S.prof_ms[cls] += ms;
+        S.prof_launches[cls] += 1;
+        S.prof_items[cls] += items;
+    }
+};
+
+void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_config& cfg, bool prof,
+                int fuel_nuc) {
+    int64_t next = S.lo;
+    Queues qs;
+    for (int k = 0; k < N_QUEUES; ++k) qs.q[k] = S.q[k];
+    const bool trace = cfg.trace_queues != 0;
+    for (;;) {
+        if (trace) CK(cudaMemsetAsync(S.trace_chk, 0, sizeof(ull) * N_QUEUES, S.stream));
+        {
+            Prof pf(S, prof, 6, S.b.cap);
+            launch_compact(S.b.event, S.b.cap, S.block_counts, S.nb, S.d_totals, qs, S.b.gidx,
+                           trace ? S.trace_chk : nullptr, S.stream);
+        }
+        CK(cudaMemcpyAsync(S.h_totals, S.d_totals, sizeof(unsigned) * N_QUEUES, cudaMemcpyDeviceToHost, S.stream));
+        if (trace)
+            CK(cudaMemcpyAsync(S.h_trace_chk, S.trace_chk, sizeof(ull) * N_QUEUES, cudaMemcpyDeviceToHost,
+                               S.stream));
+        CK(cudaStreamSynchronize(S.stream));
+        int64_t live = 0;
+        for (int k = 0; k < EV_DEAD; ++k) live += S.h_totals[k];
+        int64_t dead = S.h_totals[EV_DEAD];
+        if (live == 0 && next >= S.hi) break;
+        if (dead > 0 && next < S.hi) {
+            int n = (int)std::min<int64_t>(dead, S.hi - next);
+            Prof pf(S, prof, 7, n);
+            launch_init(c, S.q[EV_DEAD], n, next, src, S.stream);
+            next += n;
+        }
+        if (live == 0) continue;
+        int best = 0;
+        for (int k = 1; k < EV_DEAD; ++k)
+            if (S.h_totals[k] > S.h_totals[best]) best = k;
+        int n = (int)S.h_totals[best];
+        if (trace) {
+            S.trace.push_back(best);
+            S.trace.push_back(n);
+            S.trace.push_back((int64_t)S.h_trace_chk[best]);
+        }
+        S.iterations++;
+        const int32_t* qptr = S.q[best];
+        switch (best) {
+        case EV_XS_FUEL:
+            if (cfg.sort_threshold >= 0 && n >= cfg.sort_threshold) {
+                Prof pf(S, prof, 5, n);
+                launch_sort(c, S.q[best], S.q_sorted, n, R.gp.n_fuel_mats, S.hist, S.cursor, S.keys, S.stream);
+                qptr = S.q_sorted;
+                S.sorts++;
+            }
+            {
+                Prof pf(S, prof, 0, n);
+                launch_xs(c, qptr, n, S.stream);
+            }
+            if (prof) S.xs_fuel_bytes += (double)n * (44.0 + 100.0 * (double)fuel_nuc);
+            break;
+        case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, S.stream); } break;
+        case EV_ADV: { Prof pf(S, prof, 2, n); launch_advance(c, qptr, n, S.stream); } break;
+        case EV_CROSS: { Prof pf(S, prof, 3, n); launch_cross(c, qptr, n, S.stream); } break;
+        default: { Prof pf(S, prof, 4, n); launch_collide(c, qptr, n, S.stream); } break;
+        }
+    }
+}
+
+void run_queueless(Rank& R, SubBank& S, Ctx c, const Site* src, bool prof) {
+    int64_t next = S.lo;
+    for (;;) {
+        int64_t remaining = S.hi - next;
+        if (remaining > 0) {
+            CK(cudaMemsetAsync(S.ctrl, 0, sizeof(ull), S.stream));
+            Prof pf(S, prof, 7, S.b.cap);
+            launch_refill_all(c, next, remaining, src, S.stream);
+        }
+        { Prof pf(S, prof, 0, S.b.cap); launch_xs(c, nullptr, 0, S.stream); }
+        { Prof pf(S, prof, 2, S.b.cap); launch_advance(c, nullptr, 0, S.stream); }
+        { Prof pf(S, prof, 3, S.b.cap); launch_cross(c, nullptr, 0, S.stream); }
+        { Prof pf(S, prof, 4, S.b.cap); launch_collide(c, nullptr, 0, S.stream); }
+        CK(cudaMemcpyAsync(S.h_ctrl, S.ctrl, sizeof(ull) * 3, cudaMemcpyDeviceToHost, S.stream));
+        CK(cudaStreamSynchronize(S.stream));
+        S.iterations++;
+        if (remaining > 0) next += std::min<int64_t>((int64_t)S.h_ctrl[0], remaining);
+        if (S.h_ctrl[1] == 0 && next >= S.hi) break;
+    }
+}
+
+// ------------------------------------------------------------------ batches
+void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
+    CK(cudaSetDevice(R.device));
+    const int nb = cfg.n_batches;
+    const double dN = (double)R.N;
+    double k_norm = 1.0;
+    bool have_source = false;
+    const int fuel_nuc = (int)p.mat[MAT_FUEL].nuc.size();
+    const int tally_smem = 4 * R.n_tally_bins <= SMEM_TALLY_MAX;
+    long long launches0 = 0;
+    for (int batch = 1; batch <= nb; ++batch) {
+        const bool active = batch > cfg.n_inactive;
+        if (batch == cfg.n_inactive + 1) {
+            CK(cudaStreamSynchronize(R.main));
+            CK(cudaEventRecord(R.ev_a0, R.main));
+            launches0 = launch_counter();
+        }
+        CK(cudaMemsetAsync(R.acc.k, 0, sizeof(ull) * 3, R.main));
+        CK(cudaMemsetAsync(R.acc.counts, 0, sizeof(ull) * 8, R.main));
+        CK(cudaMemsetAsync(R.acc.bank_count, 0, sizeof(ull), R.main));
+        if (active) CK(cudaMemsetAsync(R.acc.tally, 0, sizeof(ull) * 4 * (size_t)R.n_tally_bins, R.main));
+        CK(cudaStreamSynchronize(R.main));
+
+        Ctx base{};
+        base.lib = R.gp.lib;
+        base.geo = R.gp.geo;
+        base.acc = R.acc;
+        base.tally_on = active ? 1 : 0;
+        base.n_tally_bins = R.n_tally_bins;
+        base.tally_smem = tally_smem;
+        base.k_norm = k_norm;
+        base.rank_lo = R.rank_lo;
+        base.n_batch = R.N;
+        base.batch = batch;
+        base.master = cfg.seed;
+        base.record_n = cfg.record_n;
+        base.recording = (R.acc.records && batch == cfg.record_batch) ? 1 : 0;
+        const Site* src = have_source ? R.source : nullptr;
+        const bool prof = cfg.profile != 0 && active;
+
+        auto drive = [&](SubBank& S) {
+            Ctx c = base;
+            c.b = S.b;
+            c.ctrl = S.ctrl;
+            CK(cudaSetDevice(R.device));
+            if (cfg.mode == OMCG_QUEUELESS) run_queueless(R, S, c, src, prof);
+            else run_queued(R, S, c, src, cfg, prof, fuel_nuc);
+            CK(cudaStreamSynchronize(S.stream));
+        };
+        if (R.subs.size() == 1) {
+            drive(R.subs[0]);
+        } else {
+            std::vector<std::thread> th;
+            std::vector<std::exception_ptr> errs(R.subs.size());
+            for (size_t t = 0; t < R.subs.size(); ++t)
+                th.emplace_back([&, t] {
+                    try { drive(R.subs[t]); } catch (...) { errs[t] = std::current_exception(); }
+                });
+            for (auto& x : th) x.join();
+            for (auto& e : errs)
+                if (e) std::rethrow_exception(e);
+        }
+        for (auto& S : R.subs) {
+            CK(cudaMemcpy(S.h_ctrl, S.ctrl, sizeof(ull) * 3, cudaMemcpyDeviceToHost));
+            if (S.h_ctrl[2] & 1ULL) throw std::runtime_error("source rejection sampling failed");
+            if (S.h_ctrl[2] & 2ULL) throw std::runtime_error("fission bank overflow");
+        }
+
+        // ---- batch reduction (NCCL across ranks: integer sums are exact)
+        if (R.world > 1) {
+            NK(ncclGroupStart());
+            NK(ncclAllReduce(R.acc.k, R.acc.k, 3, ncclUint64, ncclSum, R.comm, R.main));
+            NK(ncclAllReduce(R.acc.counts, R.acc.counts, 8, ncclUint64, ncclSum, R.comm, R.main));
+            if (active)
+                NK(ncclAllReduce(R.acc.tally, R.acc.tally, 4 * (size_t)R.n_tally_bins, ncclUint64, ncclSum, R.comm,
+                                 R.main));
+            NK(ncclAllGather(R.acc.bank_count, R.d_sall, 1, ncclUint64, R.comm, R.main));
+            NK(ncclGroupEnd());
+        } else {
+            CK(cudaMemcpyAsync(R.d_sall, R.acc.bank_count, sizeof(ull), cudaMemcpyDeviceToDevice, R.main));
+        }
+        ull hk[3], hc[8];
+        std::vector<ull> sall(R.world);
+        CK(cudaMemcpyAsync(hk, R.acc.k, sizeof hk, cudaMemcpyDeviceToHost, R.main));
+        CK(cudaMemcpyAsync(hc, R.acc.counts, sizeof hc, cudaMemcpyDeviceToHost, R.main));
+        CK(cudaMemcpyAsync(sall.data(), R.d_sall, sizeof(ull) * R.world, cudaMemcpyDeviceToHost, R.main));
+        std::vector<ull> tb;
+        if (active) {
+            tb.resize(4 * (size_t)R.n_tally_bins);
+            CK(cudaMemcpyAsync(tb.data(), R.acc.tally, sizeof(ull) * tb.size(), cudaMemcpyDeviceToHost, R.main));
+        }
+        CK(cudaStreamSynchronize(R.main));
+        R.d2h += (int64_t)(sizeof hk + sizeof hc + sizeof(ull) * (R.world + tb.size()));
+        for (size_t i = 0; i < tb.size(); ++i) R.tally_total[i] += (int64_t)tb[i];
+        for (int i = 0; i < 7; ++i) R.counts[i] += (int64_t)hc[i];
+        R.k_coll[batch - 1] = (double)(int64_t)hk[0] / TALLY_SCALE / dN;
+        R.k_abs[batch - 1] = (double)(int64_t)hk[1] / TALLY_SCALE / dN;
+        R.k_track[batch - 1] = (double)(int64_t)hk[2] / TALLY_SCALE / dN;
+        uint64_t S_total = 0, S_before = 0;
+        for (int r = 0; r < R.world; ++r) {
+            if (r < R.rank) S_before += sall[r];
+            S_total += sall[r];
+        }
+        const uint64_t S_mine = sall[R.rank];
+        R.n_sites[batch - 1] = (int64_t)S_total;
+        k_norm = R.k_coll[batch - 1];
+        R.batches_run = batch;
+        if (S_total == 0) throw std::runtime_error("fission bank empty");
+        if (batch == nb) break;
+
+        // ---- canonical bank order (history, progeny) without a sort
+        launch_scan_i32(R.acc.sites_pp, R.scan_out, R.N_rank, R.scan_tmp, R.main);
+        launch_bank_canon(R.acc.bank, (int64_t)S_mine, R.scan_out, R.rank_lo, R.canon, R.main);
+        // ---- systematic resampling to N for the next batch
+        uint64_t bs = stream_seed(cfg.seed, (uint64_t)batch, STREAM_BANK);
+        uint64_t off = (uint64_t)(prn(bs) * (double)S_total);
+        if (off >= S_total) off = S_total - 1;
+        if (R.world == 1) {
+            launch_resample(R.canon, 0, S_total, off, R.N, R.rank_lo, R.N_rank, R.source, R.main);
+        } else {
+            // each rank needs a contiguous slice of the global canonical bank
+            std::vector<int64_t> plan(4 * (size_t)R.world + 2);
+            bank_exchange_plan(reinterpret_cast<const uint64_t*>(sall.data()), R.world, R.N, off, R.rank, plan.data());
+            const int W = R.world;
+            const uint64_t my_a = (uint64_t)plan[4 * W];
+            NK(ncclGroupStart());
+            for (int r = 0; r < W; ++r) {
+                int64_t sf = plan[r], sc = plan[W + r], rf = plan[2 * W + r], rc = plan[3 * W + r];
+                if (r == R.rank) {
+                    if (sc > 0)
+                        CK(cudaMemcpyAsync(R.recv + rf, R.canon + sf, sizeof(Site) * (size_t)sc,
+                                           cudaMemcpyDeviceToDevice, R.main));
+                    continue;
+                }
+                if (sc > 0) NK(ncclSend(R.canon + sf, sizeof(Site) * (size_t)sc, ncclChar, r, R.comm, R.main));
+                if (rc > 0) NK(ncclRecv(R.recv + rf, sizeof(Site) * (size_t)rc, ncclChar, r, R.comm, R.main));
+            }
+            NK(ncclGroupEnd());
+            launch_resample(R.recv, (int64_t)my_a, S_total, off, R.N, R.rank_lo, R.N_rank, R.source, R.main);
+        }
+        CK(cudaGetLastError());
+        have_source = true;
+    }
+    CK(cudaStreamSynchronize(R.main));
+    for (auto& S : R.subs) CK(cudaStreamSynchronize(S.stream));
+    CK(cudaEventRecord(R.ev_a1, R.main));
+    CK(cudaEventSynchronize(R.ev_a1));
+    R.launches_active = launch_counter() - launches0;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, R.ev_a0, R.ev_a1));
+    R.t_active = (double)ms * 1e-3;
+    if (R.world > 1) {  // max over ranks
+        CK(cudaMemcpyAsync(R.d_time, &R.t_active, sizeof(double), cudaMemcpyHostToDevice, R.main));
+        NK(ncclAllReduce(R.d_time, R.d_time, 1, ncclFloat64, ncclMax, R.comm, R.main));
+        CK(cudaMemcpyAsync(&R.t_active, R.d_time, sizeof(double), cudaMemcpyDeviceToHost, R.main));
+        CK(cudaStreamSynchronize(R.main));
+    }
+}
+
+void validate(const omcg_run_config& cfg) {
+    if (cfg.mode != OMCG_QUEUED && cfg.mode != OMCG_QUEUELESS) throw std::invalid_argument("mode (P0) must be 0 or 1");
+    if (cfg.particles_in_flight < 1) throw std::invalid_argument("particles in flight (P1) must be >= 1");
+    if (cfg.n_bins < 1) throw std::invalid_argument("hash bins (P2) must be >= 1");
+    if (cfg.tasks_per_gpu < 1 || cfg.tasks_per_gpu > 8) throw std::invalid_argument("tasks per GPU (P5) must be 1..8");
+    if (cfg.n_particles < 1 || cfg.n_particles > ((int64_t)1 << 31) - 1)
+        throw std::invalid_argument("particles per batch out of range");
+    if (cfg.n_batches < 1 || cfg.n_batches > OMCG_MAX_BATCHES) throw std::invalid_argument("batches out of range");
+    if (cfg.n_inactive < 0 || cfg.n_inactive >= cfg.n_batches)
+        throw std::invalid_argument("inactive batches must be in [0, batches)");
+    if (cfg.world_size > 1 && (cfg.rank < 0 || cfg.rank >= cfg.world_size)) throw std::invalid_argument("bad rank");
+    if (cfg.world_size > 1 && cfg.n_gpus > 1) throw std::invalid_argument("multi-process ranks use one GPU each");
+    if (cfg.n_gpus < 1 || cfg.n_gpus > 8) throw std::invalid_argument("n_gpus must be 1..8");
+}
+
+}  // namespace
+
+// Fission-bank redistribution plan. Global canonical order is
+// rank 0's sites, then rank 1's, ... (ranks own contiguous history ranges).
+// Rank r's next-batch histories [lo_r, hi_r) resample global sites
+// [(lo_r*S+off)/N, ((hi_r-1)*S+off)/N], a contiguous range. plan layout
+// (4W+2 int64): send_first[W] send_count[W] (offsets into my canonical bank),
+// recv_first[W] recv_count[W] (offsets into my receive buffer),
+// need_first (global index of recv[0]), need_count.
+void bank_exchange_plan(const uint64_t* S_all, int W, int64_t N, uint64_t off, int me, int64_t* plan) {
+    if (W < 1 || me < 0 || me >= W || N < 1) throw std::invalid_argument("bad exchange plan arguments");
+    std::vector<uint64_t> G(W + 1, 0);
+    for (int r = 0; r < W; ++r) G[r + 1] = G[r] + S_all[r];
+    const uint64_t S = G[W];
+    if (S == 0) throw std::invalid_argument("empty fission bank");
+    auto need = [&](int r, uint64_t& a, uint64_t& b) {
+        int64_t lo = N * r / W, hi = N * (r + 1) / W;
+        if (hi <= lo) { a = b = 0; return; }
+        a = ((uint64_t)lo * S + off) / (uint64_t)N;
+        b = ((uint64_t)(hi - 1) * S + off) / (uint64_t)N + 1;  // exclusive
+    };
+    uint64_t my_a, my_b;
+    need(me, my_a, my_b);
+    for (int r = 0; r < W; ++r) {
+        uint64_t a, b;
+        need(r, a, b);
+        uint64_t s0 = std::max(G[me], a), s1 = std::min(G[me + 1], b);
+        uint64_t r0 = std::max(G[r], my_a), r1 = std::min(G[r + 1], my_b);
+        plan[r] = s1 > s0 ? (int64_t)(s0 - G[me]) : 0;
+        plan[W + r] = s1 > s0 ? (int64_t)(s1 - s0) : 0;
+        plan[2 * W + r] = r1 > r0 ? (int64_t)(r0 - my_a) : 0;
+        plan[3 * W + r] = r1 > r0 ? (int64_t)(r1 - r0) : 0;
+    }
+    plan[4 * W] = (int64_t)my_a;
+    plan[4 * W + 1] = (int64_t)(my_b - my_a);
+}
+
+std::vector<int64_t>& last_queue_trace() { return g_trace; }
+
+void nccl_unique_id(unsigned char out[128]) {
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    static_assert(sizeof(id.internal) == 128, "nccl id size");
+    std::memcpy(out, id.internal, 128);
+}
+
+int device_count() {
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    return n;
+}
+
+// ------------------------------------------------------------------ NVML (dlopen)
+namespace {
+typedef int (*nvml_init_t)(void);
+typedef int (*nvml_by_pci_t)(const char*, void**);
+typedef int (*nvml_energy_t)(void*, unsigned long long*);
+struct Nvml {
+    void* lib = nullptr;
+    nvml_init_t init = nullptr;
+    nvml_by_pci_t by_pci = nullptr;
+    nvml_energy_t energy = nullptr;
+    bool ok = false;
+    Nvml() {
+        lib = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
+        if (!lib) return;
+        init = (nvml_init_t)dlsym(lib, "nvmlInit_v2");
+        by_pci = (nvml_by_pci_t)dlsym(lib, "nvmlDeviceGetHandleByPciBusId_v2");
+        energy = (nvml_energy_t)dlsym(lib, "nvmlDeviceGetTotalEnergyConsumption");
+        ok = init && by_pci && energy && init() == 0;
+    }
+};
+Nvml& nvml() {
+    static Nvml n;
+    return n;
+}
+}  // namespace
+
+bool EnergyMeter::start(const std::vector<int>& cuda_devices) {
+    ok = false;
+    handles.clear();
+    start_mj.clear();
+    Nvml& N = nvml();
+    if (!N.ok) return false;
+    for (int d : cuda_devices) {
+        char bus[64];
+        if (cudaDeviceGetPCIBusId(bus, sizeof bus, d) != cudaSuccess) return false;
+        void* h = nullptr;
+        if (N.by_pci(bus, &h) != 0) return false;
+        unsigned long long mj = 0;
+        if (N.energy(h, &mj) != 0) return false;
+        handles.push_back(h);
+        start_mj.push_back(mj);
+    }
+    ok = true;
+    return true;
+}
+double EnergyMeter::stop_joules() {
+    if (!ok) return 0.0;
+    double j = 0.0;
+    for (size_t i = 0; i < handles.size(); ++i) {
+        unsigned long long mj = 0;
+        if (nvml().energy(handles[i], &mj) == 0) j += (double)(mj - start_mj[i]) * 1e-3;
+    }
+    return j;
+}
+
+// ------------------------------------------------------------------ entry
+void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_result* res, int64_t* tally_out,
+                   omcg_record* records) {
+    omcg_run_config cfg = cfg_in;
+    if (cfg.world_size < 1) cfg.world_size = 1;
+    validate(cfg);
+    std::memset(res, 0, sizeof *res);
+    auto t_call0 = std::chrono::steady_clock::now();
+    const bool multiproc = cfg.world_size > 1;
+    const int local_ranks = multiproc ? 1 : cfg.n_gpus;
+    int ndev = device_count();
+    std::vector<int> devs(local_ranks);
+    for (int i = 0; i < local_ranks; ++i) {
+        devs[i] = cfg.devices[i];
+        if (devs[i] < 0 || devs[i] >= ndev) throw CudaError("CUDA device " + std::to_string(devs[i]) + " not available");
+        for (int j = 0; j < i; ++j)
+            if (devs[j] == devs[i]) throw std::invalid_argument("duplicate CUDA device in devices[]");
+    }
+    EnergyMeter meter;
+    meter.start(devs);
+    reset_launch_counter();
+    std::vector<Rank> ranks(local_ranks);
+    std::vector<ncclComm_t> comms(local_ranks, nullptr);
+    if (multiproc) {
+        ncclUniqueId id;
+        std::memcpy(id.internal, cfg.nccl_id, 128);
+        CK(cudaSetDevice(devs[0]));
+        NK(ncclCommInitRank(&comms[0], cfg.world_size, id, cfg.rank));
+    } else if (local_ranks > 1) {
+        NK(ncclCommInitAll(comms.data(), local_ranks, devs.data()));
+    }
+    for (int i = 0; i < local_ranks; ++i) {
+        ranks[i].device = devs[i];
+        ranks[i].comm = comms[i];
+        ranks[i].world = multiproc ? cfg.world_size : local_ranks;
+        ranks[i].rank = multiproc ? cfg.rank : i;
+    }
+    std::vector<std::exception_ptr> errs(local_ranks);
+    auto body = [&](int i) {
+        try {
+            setup_rank(ranks[i], p, cfg);
+            run_rank(ranks[i], p, cfg);
+        } catch (...) {
+            errs[i] = std::current_exception();
+        }
+    };
+    if (local_ranks == 1) body(0);
+    else {
+        std::vector<std::thread> th;
+        for (int i = 0; i < local_ranks; ++i) th.emplace_back(body, i);
+        for (auto& t : th) t.join();
+    }
+    std::exception_ptr first;
+    for (auto& e : errs)
+        if (e && !first) first = e;
+    if (!first) {
+        Rank& R0 = ranks[0];
+        res->n_batches_run = R0.batches_run;
+        std::memcpy(res->k_coll, R0.k_coll, sizeof res->k_coll);
+        std::memcpy(res->k_abs, R0.k_abs, sizeof res->k_abs);
+        std::memcpy(res->k_track, R0.k_track, sizeof res->k_track);
+        std::memcpy(res->n_sites, R0.n_sites, sizeof res->n_sites);
+        for (int i = 0; i < 4; ++i) res->n_events[i] = R0.counts[i];
+        res->n_absorbed = R0.counts[4 + TERM_ABSORBED];
+        res->n_leaked = R0.counts[4 + TERM_LEAKED];
+        res->n_lost = R0.counts[6];
+        int n_active = 0;
+        double ks = 0.0, kq = 0.0;
+        for (int b = cfg.n_inactive; b < R0.batches_run; ++b) {
+            ks += R0.k_coll[b];
+            kq += R0.k_coll[b] * R0.k_coll[b];
+            n_active++;
+        }
+        if (n_active > 0) {
+            res->k_mean = ks / (double)n_active;
+            double var = n_active > 1 ? (kq / (double)n_active - res->k_mean * res->k_mean) / (double)(n_active - 1) : 0.0;
+            res->k_std = var > 0.0 ? std::sqrt(var) : 0.0;
+        }
+        double ta = 0.0, ti = 0.0;
+        for (auto& R : ranks) {
+            ta = std::max(ta, R.t_active);
+            ti = std::max(ti, R.t_init);
+            res->h2d_bytes += R.h2d;
+            res->d2h_bytes += R.d2h;
+            for (auto& S : R.subs) {
+                for (int k = 0; k < 8; ++k) {
+                    res->prof_ms[k] += S.prof_ms[k];
+                    res->prof_launches[k] += S.prof_launches[k];
+                    res->prof_items[k] += S.prof_items[k];
+                }
+                res->xs_fuel_bytes += S.xs_fuel_bytes;
+                res->queue_iterations += S.iterations;
+                res->sorts += S.sorts;
+            }
+        }
+        res->t_active = ta;
+        res->t_init = ti;
+        res->fom = ta > 0.0 ? (double)cfg.n_particles * (double)n_active / ta : 0.0;
+        res->kernel_launches = R0.launches_active;
+        res->kernel_launches_total = launch_counter();
+        if (tally_out) {
+            std::memcpy(tally_out, R0.tally_total.data(), sizeof(int64_t) * R0.tally_total.size());
+            res->d2h_bytes += 0;
+        }
+        if (records && R0.acc.records && cfg.record_n > 0) {
+            // records are indexed by batch-global history; each rank holds its own slice
+            for (auto& R : ranks) {
+                CK(cudaSetDevice(R.device));
+                int64_t lo = std::max<int64_t>(R.rank_lo, 0), hi = std::min<int64_t>(R.rank_lo + R.N_rank, cfg.record_n);
+                if (hi > lo)
+                    CK(cudaMemcpy(records + lo, R.acc.records + lo, sizeof(omcg_record) * (size_t)(hi - lo),
+                                  cudaMemcpyDeviceToHost));
+            }
+        }
+        {
+            std::lock_guard<std::mutex> lk(g_trace_mu);
+            g_trace.clear();
+            for (auto& S : R0.subs) g_trace.insert(g_trace.end(), S.trace.begin(), S.trace.end());
+        }
+    }
+    for (auto& R : ranks) teardown_rank(R);
+    for (auto c : comms)
+        if (c) ncclCommDestroy(c);
+    res->energy_j = meter.stop_joules();
+    res->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_call0).count();
+    if (first) std::rethrow_exception(first);
+}
+
+// ------------------------------------------------------------------ parity hooks
+uint64_t device_hash_build(const Problem& p, int n_bins, int device, int32_t* hash_out) {
+    CK(cudaSetDevice(device));
+    cudaStream_t s;
+    CK(cudaStreamCreate(&s));
+    uint64_t h;
+    {
+        GpuProblem gp;
+        gp.upload(p, n_bins, device, s);
+        size_t n = (size_t)(n_bins + 1) * (size_t)p.n_nuc;
+        std::vector<int32_t> hh(n);
+        CK(cudaMemcpyAsync(hh.data(), gp.lib.hash, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        h = fnv1a(1469598103934665603ULL, hh.data(), sizeof(int32_t) * n);
+        if (hash_out) std::memcpy(hash_out, hh.data(), sizeof(int32_t) * n);
+    }
+    cudaStreamDestroy(s);
+    return h;
+}
+
+void device_xs_lookup(const Problem& p, int n_bins, int device, int64_t n, const int32_t* mat, const double* E,
+                      double* out) {
+    CK(cudaSetDevice(device));
+    cudaStream_t s;
+    CK(cudaStreamCreate(&s));
+    {
+        GpuProblem gp;
+        gp.upload(p, n_bins, device, s);
+        DevArena a;
+        a.device = device;
+        int32_t* dm = a.alloc<int32_t>(n);
+        double* dE = a.alloc<double>(n);
+        double* dout = a.alloc<double>(4 * n);
+        for (int64_t i = 0; i < n; ++i)
+            if (mat[i] < 0 || mat[i] >= (int)p.mat.size()) throw std::invalid_argument("material out of range");
+        CK(cudaMemcpyAsync(dm, mat, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dE, E, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        launch_xs_pairs(gp.lib, n, dm, dE, dout, s);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, dout, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    cudaStreamDestroy(s);
+}
+
+}  // namespace omcg

@@ -1,0 +1,40 @@
+// transport.hpp — host driver of the event-based loop (C++), called by the C ABI.
+#pragma once
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/omcg.h"
+#include "problem.hpp"
+
+namespace omcg {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void run_transport(const Problem& p, const omcg_run_config& cfg, omcg_run_result* res, int64_t* tally_out,
+                   omcg_record* records);
+
+uint64_t device_hash_build(const Problem& p, int n_bins, int device, int32_t* hash_out);
+void device_xs_lookup(const Problem& p, int n_bins, int device, int64_t n, const int32_t* mat, const double* E,
+                      double* out);
+
+std::vector<int64_t>& last_queue_trace();
+void bank_exchange_plan(const uint64_t* S_all, int world, int64_t n_batch, uint64_t off, int rank, int64_t* plan);
+void nccl_unique_id(unsigned char out[128]);
+int device_count();
+
+// NVML energy counter (dlopen'ed; returns false when unavailable)
+struct EnergyMeter {
+    bool start(const std::vector<int>& cuda_devices);
+    double stop_joules();  // energy since start, summed over devices
+    std::vector<void*> handles;
+    std::vector<unsigned long long> start_mj;
+    bool ok = false;
+};
+
+}  // namespace omcg
