@@ -1,0 +1,251 @@
+#!/usr/bin/env python
+"""bench.py — FoM (particles/s, active batches) of the B200 event-based transport loop.
+
+Workload (BASELINE.json configs[1]): SMR-like 17x17 assembly,
+depleted fuel with 261 of 272 synthetic nuclides, 1e6 histories per batch per GPU,
+the paper's default tuning point P0=openmc (queued), P1=1e6 in flight, P2=4000
+hash bins, P3=20000 sort threshold (Table 1). A "step" is one batch.
+--warmup W inactive batches, then --steps K timed active batches.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 is launched by the driver under torchrun (one process per GPU): weak
+scaling, N x 1e6 histories per batch, NCCL only for the per-batch tally/k-eff
+reduction and fission-bank exchange. Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FoM particles/s (active batches)"
+FUEL_NUCLIDES = 261
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--problem", default="assembly", choices=["pincell", "assembly", "core"])
+    ap.add_argument("--particles", type=int, default=1_000_000, help="histories per batch per GPU")
+    ap.add_argument("--mode", default="openmc", choices=["openmc", "openmc-queueless"])
+    ap.add_argument("--in-flight", type=int, default=1_000_000)
+    ap.add_argument("--bins", type=int, default=4000)
+    ap.add_argument("--sort", type=int, default=20_000)
+    ap.add_argument("--tasks", type=int, default=1)
+    ap.add_argument("--cpu-sample", type=int, default=100_000, help="histories per CPU-baseline batch")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(a, world):
+    return {
+        "workload": f"C2 {a.problem}: SMR-like 17x17 assembly, depleted fuel (261 of 272 synthetic nuclides), "
+                    f"{a.particles} histories/batch/GPU" if a.problem == "assembly" else
+                    f"{a.problem}, {a.particles} histories/batch/GPU",
+        "P0": a.mode, "P1": a.in_flight, "P2": a.bins, "P3": a.sort if a.mode == "openmc" else None,
+        "P4": 8, "P5": a.tasks, "P6": "threads",
+        "histories_per_batch": a.particles * world,
+        "parallelism": f"particle-bank dp{world}",
+        "l2": "no flush needed: working set (122 MB library + ~170 MB in-flight bank) exceeds the 126 MB L2",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            c = [x.strip() for x in line.split(",")]
+            if len(c) < 9:
+                continue
+            try:
+                sm.append(float(c[1]))
+                mx.append(float(c[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, c[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic_per_item():
+    """dram bytes per fuel-XS queue entry from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "xs_fuel_ncu.json")) as f:
+            d = json.load(f)
+        return float(d["dram_bytes_per_item"]), d.get("source", "profiles/xs_fuel_ncu.json")
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
+def cpu_baseline(a, batches=3, inactive=1):
+    """The CPU oracle (history-based C, all host threads) on a bounded sample of the workload."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    kind = {"pincell": O.PINCELL, "assembly": O.ASSEMBLY, "core": O.CORE}[a.problem]
+    p = O.Problem(kind, 1234, a.bins)
+    res, _, _ = p.run(a.cpu_sample, batches, inactive, seed=1, threads=0)
+    cores = os.cpu_count()
+    return {"value": res.fom, "unit": "particles/s", "cores": cores, "kind": "port",
+            "sample": f"{a.problem}, {a.cpu_sample} histories/batch x {batches} batches ({inactive} inactive), "
+                      f"oracle/omc_oracle.c history-based, {cores} threads, {res.t_active:.1f} s active",
+            "k_eff": res.k_mean}
+
+
+def run_reference(a, rank):
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    kind = {"pincell": O.PINCELL, "assembly": O.ASSEMBLY, "core": O.CORE}[a.problem]
+    n = max(1000, a.cpu_sample // 2)
+    p = O.Problem(kind, 1234, a.bins)
+    t0 = time.perf_counter()
+    res, _, _ = p.run(n, a.warmup + a.steps, a.warmup, seed=1, threads=0)
+    wall = time.perf_counter() - t0
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res.fom, "unit": "particles/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * res.t_active / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded library xs_seed=1234, transport seed=1)",
+        "config": workload_config(a, 1),
+        "cpu_baseline": {"value": res.fom, "unit": "particles/s", "cores": cores, "kind": "port",
+                         "sample": f"{n} histories/batch x {a.warmup + a.steps} batches on the host CPU "
+                                   "(the reference ships no transport code; this is the CPU oracle port, "
+                                   "oracle/omc_oracle.c)"},
+        "e2e": {"value": res.fom, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "k_eff": res.k_mean, "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank)
+        return
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2402_09222_b200 as P
+
+    problem = P.Problem(a.problem, host_threads=8)  # host buffers: the e2e inputs
+    nccl_id = None
+    if world > 1:
+        obj = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    sampler = ClockSampler() if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = P.run(problem, mode=a.mode, particles_in_flight=a.in_flight, n_bins=a.bins,
+                sort_threshold=a.sort if a.mode == "openmc" else None, host_threads=8, tasks_per_gpu=a.tasks,
+                n_particles=a.particles * world, n_batches=a.warmup + a.steps, n_inactive=a.warmup, seed=1,
+                world_size=world, rank=rank, nccl_id=nccl_id, devices=[local], profile=True)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    r = out.result
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    hist_total = a.particles * world * (a.warmup + a.steps)
+    peak, peak_src = peaks()
+    xs_ms = r.prof_ms[0]
+    achieved = (r.xs_fuel_bytes / (xs_ms * 1e-3) / 1e9) if xs_ms > 0 else None
+    per_item, traffic_src = ncu_traffic_per_item()
+    items_per_launch = r.prof_items[0] / max(1, r.prof_launches[0])
+    classes = ["calculate_xs_fuel", "calculate_xs_nonfuel", "advance", "surface_crossing", "collision",
+               "sort", "refill", "tail"]
+    tot_ms = sum(r.prof_ms[i] for i in range(8))
+    line = {
+        "metric": METRIC, "value": r.fom, "unit": "particles/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1e3 * r.t_active / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded library xs_seed=1234, transport seed=1)",
+        "config": workload_config(a, world),
+        "e2e": {"value": hist_total / wall, "unit": "particles/s",
+                "h2d_bytes_per_step": int(r.h2d_bytes / (a.warmup + a.steps)),
+                "d2h_bytes_per_step": int(r.d2h_bytes / (a.warmup + a.steps)),
+                "what": "omcg_run through the C ABI from host buffers: library upload + hash build + all "
+                        f"{a.warmup + a.steps} batches + result readback, wall clock (max over ranks)"},
+        "roofline": {"bound": "hbm", "kernel": "calculate_xs (fuel queue)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": (per_item * items_per_launch) if per_item else None,
+                     "algorithmic_bytes_per_lookup": 44 + 100 * FUEL_NUCLIDES,
+                     "items_per_launch": items_per_launch, "launches": r.prof_launches[0],
+                     "peak_source": peak_src, "traffic_source": traffic_src},
+        "kernel_share": {classes[i]: round(r.prof_ms[i] / tot_ms, 4) for i in range(8)} if tot_ms else None,
+        "gpu_launches": r.kernel_launches,
+        "clocks": clocks,
+        "k_eff": {"collision_mean": r.k_mean, "std": r.k_std},
+        "edp": {"energy_j": r.energy_j, "t_total_s": r.t_total, "edp_js": r.energy_j * r.t_total},
+        "t_init_s": r.t_init, "queue_iterations": r.queue_iterations, "sorts": r.sorts,
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(a)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -92,6 +92,10 @@ typedef struct {
     int64_t record_n;
     int profile;                  /* time every kernel class with CUDA events */
     int trace_queues;             /* record per-iteration (queue, length, id-checksum) */
+    /* When the source is exhausted and at most tail_threshold histories are
+     * alive, finish them in one history-per-thread launch instead of one
+     * launch per event (results are identical; 0 disables). */
+    int64_t tail_threshold;
 } omcg_run_config;
 
 typedef struct {
@@ -117,12 +121,13 @@ typedef struct {
     int64_t kernel_launches_total;
     int64_t h2d_bytes, d2h_bytes; /* host<->device traffic of the call */
     /* profile (profile != 0): per kernel class, active batches */
-    double prof_ms[8];            /* xs_fuel, xs_nonfuel, advance, cross, collision, sort, compact, other */
+    double prof_ms[8];            /* xs_fuel, xs_nonfuel, advance, cross, collision, sort, refill, tail */
     int64_t prof_launches[8];
     int64_t prof_items[8];        /* queue entries processed */
     double xs_fuel_bytes;         /* algorithmic bytes of the fuel XS launches */
     int64_t queue_iterations;     /* host event-loop iterations, all batches */
     int64_t sorts;                /* fuel-queue sorts performed */
+    int64_t tail_launches;        /* history-per-thread tail launches */
 } omcg_run_result;
 
 OMCG_API const char* omcg_version(void);

@@ -106,7 +106,7 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
                 host_threads=8, tasks_per_gpu=1, cpu_bind="threads", n_particles=1_000_000,
                 n_batches=15, n_inactive=5, seed=1, n_gpus=1, devices=None, world_size=1, rank=0,
                 nccl_id: bytes | None = None, record_batch=0, record_n=0, profile=False,
-                trace_queues=False) -> RunConfig:
+                trace_queues=False, tail_threshold=None) -> RunConfig:
     cfg = RunConfig()
     _lib.omcg_run_config_default(C.byref(cfg))
     cfg.mode = QUEUELESS if mode in ("openmc-queueless", "queueless", QUEUELESS) else QUEUED
@@ -132,6 +132,8 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
     cfg.record_n = int(record_n)
     cfg.profile = int(bool(profile))
     cfg.trace_queues = int(bool(trace_queues))
+    if tail_threshold is not None:
+        cfg.tail_threshold = int(tail_threshold)
     return cfg
 
 

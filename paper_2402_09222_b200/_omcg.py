@@ -44,7 +44,7 @@ class RunConfig(C.Structure):
         ("n_inactive", C.c_int), ("seed", C.c_uint64), ("n_gpus", C.c_int),
         ("devices", C.c_int * 8), ("world_size", C.c_int), ("rank", C.c_int),
         ("nccl_id", C.c_ubyte * 128), ("record_batch", C.c_int), ("record_n", C.c_int64),
-        ("profile", C.c_int), ("trace_queues", C.c_int),
+        ("profile", C.c_int), ("trace_queues", C.c_int), ("tail_threshold", C.c_int64),
     ]
 
 
@@ -67,6 +67,7 @@ class RunResult(C.Structure):
         ("kernel_launches_total", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
         ("prof_ms", C.c_double * 8), ("prof_launches", C.c_int64 * 8), ("prof_items", C.c_int64 * 8),
         ("xs_fuel_bytes", C.c_double), ("queue_iterations", C.c_int64), ("sorts", C.c_int64),
+        ("tail_launches", C.c_int64),
     ]
 
 

@@ -129,6 +129,7 @@ OMCG_API void omcg_run_config_default(omcg_run_config* c) {
     for (int i = 0; i < 8; ++i) c->devices[i] = i;
     c->world_size = 1;
     c->rank = 0;
+    c->tail_threshold = 16384;
 }
 
 OMCG_API int omcg_run(const omcg_problem* p, const omcg_run_config* cfg, omcg_run_result* res, int64_t* tally_out,

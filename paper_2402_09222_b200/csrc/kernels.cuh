@@ -6,8 +6,20 @@
 
 namespace omcg {
 
+// Event queues of one sub-bank: N_QUEUES int32 lists of `cap` entries,
+// contiguous (queue t at qbase + t*cap). Lengths of the live queues in
+// count[0..4]; the dead queue is a ring whose tail lives on the device.
+struct QueueSet {
+    int32_t* qbase;
+    int64_t cap;
+    unsigned* count;
+    unsigned long long* dead_tail;
+};
+
 // Everything an event kernel needs, passed by value as the kernel parameter.
 struct Ctx {
+    QueueSet qs;
+    unsigned long long* trace_chk;  // per-launch order-free checksum of processed histories
     DevLib lib;
     Geometry geo;  // geo.pin_map is a device pointer
     Bank b;
@@ -25,10 +37,6 @@ struct Ctx {
     unsigned long long* ctrl;  // [0] refill ticket, [1] alive, [2] error flags
 };
 
-struct Queues {
-    int32_t* q[N_QUEUES];
-};
-
 constexpr int SMEM_TALLY_MAX = 2048;  // tally bins*scores aggregated per block in smem
 
 // bookkeeping
@@ -40,23 +48,19 @@ void launch_hash_build(const DevLib& lib, int32_t* hash, cudaStream_t s);
 void launch_xs_pairs(const DevLib& lib, int64_t n, const int32_t* mat, const double* E, double* out,
                      cudaStream_t s);
 
-// queue compaction (deterministic, slot order)
-void launch_compact(const int8_t* event, int64_t cap, int32_t* block_counts, int nb, unsigned int* totals,
-                    Queues qs, const int32_t* gidx, unsigned long long* trace_chk, cudaStream_t s);
-
 // event kernels; q == nullptr selects the queueless variant over all cap slots
-void launch_init(const Ctx& c, const int32_t* dead_q, int n, int64_t first_local, const Site* src,
-                 cudaStream_t s);
+void launch_init(const Ctx& c, uint64_t head, int n, int64_t first_local, const Site* src, cudaStream_t s);
+void launch_tail(const Ctx& c, bool queued, cudaStream_t s);
 void launch_refill_all(const Ctx& c, int64_t first_local, int64_t n_remaining, const Site* src,
                        cudaStream_t s);
-void launch_xs(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
+void launch_xs(const Ctx& c, const int32_t* q, int n, bool fuel, cudaStream_t s);
 void launch_advance(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 void launch_cross(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 void launch_collide(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 
 // material/energy sort of the fuel XS queue (16-bit energy radix per material)
 void launch_sort(const Ctx& c, const int32_t* q_in, int32_t* q_out, int n, int n_fuel_mats,
-                 unsigned int* hist, unsigned int* cursor, uint32_t* keys, cudaStream_t s);
+                 unsigned int* hist, unsigned int* cursor, uint32_t* keys, unsigned int* bsum, cudaStream_t s);
 
 // fission bank: canonical order + systematic resampling
 void launch_scan_i32(const int32_t* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);

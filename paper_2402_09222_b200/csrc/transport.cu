@@ -140,23 +140,29 @@ struct GpuProblem {
 struct SubBank {
     cudaStream_t stream = nullptr;
     Bank b{};
-    int32_t* q[N_QUEUES] = {};
+    QueueSet qs{};
     int32_t* q_sorted = nullptr;
     uint32_t* keys = nullptr;
     unsigned* hist = nullptr;
     unsigned* cursor = nullptr;
-    int32_t* block_counts = nullptr;
-    int nb = 0;
-    unsigned* d_totals = nullptr;
-    unsigned* h_totals = nullptr;  // pinned
+    unsigned* bsum = nullptr;
+    unsigned* h_counts = nullptr;  // pinned: live queue lengths [0..4], then dead tail (as 2 words)
+    uint64_t dead_head = 0;        // ring head (host side; only the refill consumes)
     ull* ctrl = nullptr;           // [0] ticket [1] alive [2] errors
     ull* h_ctrl = nullptr;         // pinned
     ull* trace_chk = nullptr;
     ull* h_trace_chk = nullptr;
     int64_t lo = 0, hi = 0;        // rank-local history range
+    int64_t tail_launches = 0;
     std::vector<int64_t> trace;
     // profile
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    struct EvPair {
+        cudaEvent_t a = nullptr, b = nullptr;
+        int cls = 0;
+        int64_t items = 0;
+    };
+    std::vector<EvPair> evs;  // deferred per-kernel timing, read after each host sync
+    int n_pending = 0;
     double prof_ms[8] = {};
     int64_t prof_launches[8] = {};
     int64_t prof_items[8] = {};
@@ -259,23 +265,38 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         B.n_xs = A.alloc<int32_t>(cap); B.n_adv = A.alloc<int32_t>(cap); B.n_cross = A.alloc<int32_t>(cap);
         B.n_coll = A.alloc<int32_t>(cap); B.n_sites = A.alloc<int32_t>(cap);
         CK(cudaMemsetAsync(B.event, EV_DEAD, (size_t)cap, S.stream));
-        for (int k = 0; k < N_QUEUES; ++k) S.q[k] = A.alloc<int32_t>(cap);
+        S.qs.cap = cap;
+        S.qs.qbase = A.alloc<int32_t>((int64_t)N_QUEUES * cap);
+        S.qs.count = A.alloc<unsigned>(8);  // [0..4] live lengths, [6..7] dead tail (u64)
+        S.qs.dead_tail = reinterpret_cast<ull*>(S.qs.count + 6);
+        {   // every slot starts in the dead ring
+            std::vector<int32_t> iota((size_t)cap);
+            for (int64_t i = 0; i < cap; ++i) iota[(size_t)i] = (int32_t)i;
+            CK(cudaMemcpy(S.qs.qbase + (int64_t)EV_DEAD * cap, iota.data(), sizeof(int32_t) * (size_t)cap,
+                          cudaMemcpyHostToDevice));
+            unsigned init_counts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            ull tail = (ull)cap;
+            std::memcpy(init_counts + 6, &tail, sizeof tail);
+            CK(cudaMemcpy(S.qs.count, init_counts, sizeof init_counts, cudaMemcpyHostToDevice));
+            S.dead_head = 0;
+        }
         S.q_sorted = A.alloc<int32_t>(cap);
         S.keys = A.alloc<uint32_t>(cap);
         S.hist = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
         S.cursor = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
+        S.bsum = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 64);
         CK(cudaMemsetAsync(S.hist, 0, sizeof(unsigned) * (size_t)R.gp.n_fuel_mats * 65536, S.stream));
-        S.nb = (int)((cap + 1023) / 1024);
-        S.block_counts = A.alloc<int32_t>((int64_t)N_QUEUES * S.nb);
-        S.d_totals = A.alloc<unsigned>(N_QUEUES);
         S.ctrl = A.alloc<ull>(4);
-        S.trace_chk = A.alloc<ull>(N_QUEUES);
+        S.trace_chk = A.alloc<ull>(1);
         CK(cudaMemsetAsync(S.ctrl, 0, sizeof(ull) * 4, S.stream));
-        CK(cudaMallocHost(&S.h_totals, sizeof(unsigned) * N_QUEUES));
+        CK(cudaMallocHost(&S.h_counts, sizeof(unsigned) * 8));
         CK(cudaMallocHost(&S.h_ctrl, sizeof(ull) * 4));
-        CK(cudaMallocHost(&S.h_trace_chk, sizeof(ull) * N_QUEUES));
-        CK(cudaEventCreate(&S.e0));
-        CK(cudaEventCreate(&S.e1));
+        CK(cudaMallocHost(&S.h_trace_chk, sizeof(ull)));
+        S.evs.resize(64);
+        for (auto& e : S.evs) {
+            CK(cudaEventCreate(&e.a));
+            CK(cudaEventCreate(&e.b));
+        }
         CK(cudaStreamSynchronize(S.stream));
     }
     CK(cudaStreamSynchronize(R.main));
@@ -286,11 +307,13 @@ void teardown_rank(Rank& R) {
     cudaSetDevice(R.device);
     for (auto& S : R.subs) {
         if (S.stream) cudaStreamDestroy(S.stream);
-        if (S.h_totals) cudaFreeHost(S.h_totals);
+        if (S.h_counts) cudaFreeHost(S.h_counts);
         if (S.h_ctrl) cudaFreeHost(S.h_ctrl);
         if (S.h_trace_chk) cudaFreeHost(S.h_trace_chk);
-        if (S.e0) cudaEventDestroy(S.e0);
-        if (S.e1) cudaEventDestroy(S.e1);
+        for (auto& e : S.evs) {
+            if (e.a) cudaEventDestroy(e.a);
+            if (e.b) cudaEventDestroy(e.b);
+        }
     }
     if (R.main) cudaStreamDestroy(R.main);
     if (R.ev_a0) cudaEventDestroy(R.ev_a0);
@@ -298,106 +321,146 @@ void teardown_rank(Rank& R) {
 }
 
 // ------------------------------------------------------------------ event loops
+// Per-kernel CUDA-event timing on the launching stream. Events are recorded
+// around each launch and read back only after the loop's next host sync, so
+// profiling adds two event records per launch and no extra synchronisation.
+void drain_profile(SubBank& S) {
+    if (S.n_pending == 0) return;
+    CK(cudaEventSynchronize(S.evs[S.n_pending - 1].b));
+    for (int i = 0; i < S.n_pending; ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, S.evs[i].a, S.evs[i].b));
+        S.prof_ms[S.evs[i].cls] += ms;
+        S.prof_launches[S.evs[i].cls] += 1;
+        S.prof_items[S.evs[i].cls] += S.evs[i].items;
+    }
+    S.n_pending = 0;
+}
+
 struct Prof {
     SubBank& S;
     bool on;
-    int cls;
-    int64_t items;
-    Prof(SubBank& s, bool enabled, int c, int64_t n) : S(s), on(enabled), cls(c), items(n) {
-        if (on) CK(cudaEventRecord(S.e0, S.stream));
+    Prof(SubBank& s, bool enabled, int cls, int64_t items) : S(s), on(enabled) {
+        if (!on) return;
+        if (S.n_pending == (int)S.evs.size()) drain_profile(S);
+        auto& e = S.evs[S.n_pending];
+        e.cls = cls;
+        e.items = items;
+        CK(cudaEventRecord(e.a, S.stream));
     }
     ~Prof() {
         if (!on) return;
-        float ms = 0.f;
-        if (cudaEventRecord(S.e1, S.stream) != cudaSuccess || cudaEventSynchronize(S.e1) != cudaSuccess ||
-            cudaEventElapsedTime(&ms, S.e0, S.e1) != cudaSuccess)
-            return;
-        S.prof_ms[cls] += ms;
-        S.prof_launches[cls] += 1;
-        S.prof_items[cls] += items;
+        if (cudaEventRecord(S.evs[S.n_pending].b, S.stream) == cudaSuccess) S.n_pending++;
     }
 };
 
 void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_config& cfg, bool prof,
                 int fuel_nuc) {
     int64_t next = S.lo;
-    Queues qs;
-    for (int k = 0; k < N_QUEUES; ++k) qs.q[k] = S.q[k];
     const bool trace = cfg.trace_queues != 0;
+    const int64_t tail = cfg.tail_threshold;
+    bool pending_trace = false;
     for (;;) {
-        if (trace) CK(cudaMemsetAsync(S.trace_chk, 0, sizeof(ull) * N_QUEUES, S.stream));
-        {
-            Prof pf(S, prof, 6, S.b.cap);
-            launch_compact(S.b.event, S.b.cap, S.block_counts, S.nb, S.d_totals, qs, S.b.gidx,
-                           trace ? S.trace_chk : nullptr, S.stream);
-        }
-        CK(cudaMemcpyAsync(S.h_totals, S.d_totals, sizeof(unsigned) * N_QUEUES, cudaMemcpyDeviceToHost, S.stream));
-        if (trace)
-            CK(cudaMemcpyAsync(S.h_trace_chk, S.trace_chk, sizeof(ull) * N_QUEUES, cudaMemcpyDeviceToHost,
-                               S.stream));
+        CK(cudaMemcpyAsync(S.h_counts, S.qs.count, sizeof(unsigned) * 8, cudaMemcpyDeviceToHost, S.stream));
+        if (pending_trace) CK(cudaMemcpyAsync(S.h_trace_chk, S.trace_chk, sizeof(ull), cudaMemcpyDeviceToHost, S.stream));
         CK(cudaStreamSynchronize(S.stream));
+        if (prof) drain_profile(S);
+        if (pending_trace) {
+            S.trace.back() = (int64_t)S.h_trace_chk[0];
+            pending_trace = false;
+        }
         int64_t live = 0;
-        for (int k = 0; k < EV_DEAD; ++k) live += S.h_totals[k];
-        int64_t dead = S.h_totals[EV_DEAD];
+        for (int k = 0; k < EV_DEAD; ++k) live += S.h_counts[k];
+        ull dead_tail;
+        std::memcpy(&dead_tail, S.h_counts + 6, sizeof dead_tail);
+        const int64_t dead = (int64_t)(dead_tail - S.dead_head);
         if (live == 0 && next >= S.hi) break;
+        if (live > 0) {
+            S.iterations++;
+            if (trace) {
+                CK(cudaMemsetAsync(S.trace_chk, 0, sizeof(ull), S.stream));
+                c.trace_chk = S.trace_chk;
+            }
+            int best = 0;
+            for (int k = 1; k < EV_DEAD; ++k)
+                if (S.h_counts[k] > S.h_counts[best]) best = k;
+            int n = (int)S.h_counts[best];
+            if (next >= S.hi && live <= tail) {
+                // sparse end of the batch: one launch finishes every live history
+                best = EV_DEAD;
+                n = (int)live;
+                Prof pf(S, prof, 7, live);
+                launch_tail(c, true, S.stream);
+                S.tail_launches++;
+            } else {
+                const int32_t* qptr = S.qs.qbase + (int64_t)best * S.qs.cap;
+                switch (best) {
+                case EV_XS_FUEL:
+                    if (cfg.sort_threshold >= 0 && n >= cfg.sort_threshold) {
+                        Prof pf(S, prof, 5, n);
+                        launch_sort(c, qptr, S.q_sorted, n, R.gp.n_fuel_mats, S.hist, S.cursor, S.keys, S.bsum,
+                                    S.stream);
+                        qptr = S.q_sorted;
+                        S.sorts++;
+                    }
+                    {
+                        Prof pf(S, prof, 0, n);
+                        launch_xs(c, qptr, n, true, S.stream);
+                    }
+                    if (prof) S.xs_fuel_bytes += (double)n * (44.0 + 100.0 * (double)fuel_nuc);
+                    break;
+                case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, false, S.stream); } break;
+                case EV_ADV: { Prof pf(S, prof, 2, n); launch_advance(c, qptr, n, S.stream); } break;
+                case EV_CROSS: { Prof pf(S, prof, 3, n); launch_cross(c, qptr, n, S.stream); } break;
+                default: { Prof pf(S, prof, 4, n); launch_collide(c, qptr, n, S.stream); } break;
+                }
+            }
+            c.trace_chk = nullptr;
+            if (trace) {
+                S.trace.push_back(best);
+                S.trace.push_back(n);
+                S.trace.push_back(0);
+                pending_trace = true;
+            }
+        }
+        // refill the in-flight bank from the dead ring
         if (dead > 0 && next < S.hi) {
             int n = (int)std::min<int64_t>(dead, S.hi - next);
-            Prof pf(S, prof, 7, n);
-            launch_init(c, S.q[EV_DEAD], n, next, src, S.stream);
+            Prof pf(S, prof, 6, n);
+            launch_init(c, S.dead_head, n, next, src, S.stream);
+            S.dead_head += (uint64_t)n;
             next += n;
-        }
-        if (live == 0) continue;
-        int best = 0;
-        for (int k = 1; k < EV_DEAD; ++k)
-            if (S.h_totals[k] > S.h_totals[best]) best = k;
-        int n = (int)S.h_totals[best];
-        if (trace) {
-            S.trace.push_back(best);
-            S.trace.push_back(n);
-            S.trace.push_back((int64_t)S.h_trace_chk[best]);
-        }
-        S.iterations++;
-        const int32_t* qptr = S.q[best];
-        switch (best) {
-        case EV_XS_FUEL:
-            if (cfg.sort_threshold >= 0 && n >= cfg.sort_threshold) {
-                Prof pf(S, prof, 5, n);
-                launch_sort(c, S.q[best], S.q_sorted, n, R.gp.n_fuel_mats, S.hist, S.cursor, S.keys, S.stream);
-                qptr = S.q_sorted;
-                S.sorts++;
-            }
-            {
-                Prof pf(S, prof, 0, n);
-                launch_xs(c, qptr, n, S.stream);
-            }
-            if (prof) S.xs_fuel_bytes += (double)n * (44.0 + 100.0 * (double)fuel_nuc);
-            break;
-        case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, S.stream); } break;
-        case EV_ADV: { Prof pf(S, prof, 2, n); launch_advance(c, qptr, n, S.stream); } break;
-        case EV_CROSS: { Prof pf(S, prof, 3, n); launch_cross(c, qptr, n, S.stream); } break;
-        default: { Prof pf(S, prof, 4, n); launch_collide(c, qptr, n, S.stream); } break;
         }
     }
 }
 
-void run_queueless(Rank& R, SubBank& S, Ctx c, const Site* src, bool prof) {
+void run_queueless(Rank& R, SubBank& S, Ctx c, const Site* src, bool prof, int64_t tail) {
     int64_t next = S.lo;
     for (;;) {
         int64_t remaining = S.hi - next;
         if (remaining > 0) {
             CK(cudaMemsetAsync(S.ctrl, 0, sizeof(ull), S.stream));
-            Prof pf(S, prof, 7, S.b.cap);
+            Prof pf(S, prof, 6, S.b.cap);
             launch_refill_all(c, next, remaining, src, S.stream);
         }
-        { Prof pf(S, prof, 0, S.b.cap); launch_xs(c, nullptr, 0, S.stream); }
+        { Prof pf(S, prof, 0, S.b.cap); launch_xs(c, nullptr, 0, false, S.stream); }
         { Prof pf(S, prof, 2, S.b.cap); launch_advance(c, nullptr, 0, S.stream); }
         { Prof pf(S, prof, 3, S.b.cap); launch_cross(c, nullptr, 0, S.stream); }
         { Prof pf(S, prof, 4, S.b.cap); launch_collide(c, nullptr, 0, S.stream); }
         CK(cudaMemcpyAsync(S.h_ctrl, S.ctrl, sizeof(ull) * 3, cudaMemcpyDeviceToHost, S.stream));
         CK(cudaStreamSynchronize(S.stream));
+        if (prof) drain_profile(S);
         S.iterations++;
         if (remaining > 0) next += std::min<int64_t>((int64_t)S.h_ctrl[0], remaining);
-        if (S.h_ctrl[1] == 0 && next >= S.hi) break;
+        const int64_t alive = (int64_t)S.h_ctrl[1];
+        if (alive == 0 && next >= S.hi) break;
+        if (next >= S.hi && alive <= tail) {
+            Prof pf(S, prof, 7, alive);
+            launch_tail(c, false, S.stream);
+            S.tail_launches++;
+            CK(cudaStreamSynchronize(S.stream));
+            break;
+        }
     }
 }
 
@@ -444,11 +507,14 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         auto drive = [&](SubBank& S) {
             Ctx c = base;
             c.b = S.b;
+            c.qs = S.qs;
             c.ctrl = S.ctrl;
+            c.trace_chk = nullptr;
             CK(cudaSetDevice(R.device));
-            if (cfg.mode == OMCG_QUEUELESS) run_queueless(R, S, c, src, prof);
+            if (cfg.mode == OMCG_QUEUELESS) run_queueless(R, S, c, src, prof, cfg.tail_threshold);
             else run_queued(R, S, c, src, cfg, prof, fuel_nuc);
             CK(cudaStreamSynchronize(S.stream));
+            drain_profile(S);
         };
         if (R.subs.size() == 1) {
             drive(R.subs[0]);
@@ -775,6 +841,7 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
                 res->xs_fuel_bytes += S.xs_fuel_bytes;
                 res->queue_iterations += S.iterations;
                 res->sorts += S.sorts;
+                res->tail_launches += S.tail_launches;
             }
         }
         res->t_active = ta;

@@ -82,6 +82,9 @@ def test_assembly_transport_bit_exact():
     dict(particles_in_flight=5000, n_bins=100000),
     dict(mode="openmc-queueless", particles_in_flight=3000),  # P0
     dict(particles_in_flight=2000, tasks_per_gpu=2),      # P5
+    dict(particles_in_flight=5000, tail_threshold=0),     # pure event-by-event
+    dict(particles_in_flight=5000, tail_threshold=10**9),  # history-per-thread tail right after refill
+    dict(mode="openmc-queueless", particles_in_flight=3000, tail_threshold=0),
 ])
 def test_tuned_parameters_do_not_change_results(kw):
     """in-flight count (and every other tuned knob) changes time only."""
