@@ -94,7 +94,7 @@ OMCG_API uint64_t omcg_library_checksum(const omcg_problem* p) {
 OMCG_API int omcg_hash_build(const omcg_problem* p, int n_bins, int device, uint64_t* checksum, int32_t* hash_out) {
     return wrap([&] {
         if (!p || !checksum) throw std::invalid_argument("null argument");
-        if (n_bins < 1 || n_bins > 10000000) throw std::invalid_argument("n_bins out of range");
+        if (n_bins < 1 || n_bins > 1000000) throw std::invalid_argument("n_bins out of range [1, 1e6]");
         *checksum = omcg::device_hash_build(p->p, n_bins, device, hash_out);
     });
 }

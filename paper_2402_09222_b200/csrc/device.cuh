@@ -27,6 +27,7 @@ struct DevLib {
     const double* awr;       // n_nuc
     const int32_t* mat_off;  // n_mat+1
     const int32_t* mat_nuc;
+    const int4* mat_desc;    // per material entry: {E offset, grid size, hash-row offset, nuclide}
     const double* mat_dens;
     const uint8_t* mat_fissionable;
     const uint8_t* mat_fuel;  // material uses the fuel XS queue
@@ -46,7 +47,13 @@ struct Bank {
     int32_t *gidx, *cell;
     int8_t *ring, *mat, *surf, *event;
     int32_t *n_xs, *n_adv, *n_cross, *n_coll, *n_sites;
+    // running macroscopic total after every CKPT_STRIDE nuclides of a large
+    // material (written by calculate_xs, read by collision to jump straight
+    // to the segment holding the sampled nuclide): NCKPT x cap
+    double* ckpt;
 };
+constexpr int CKPT_STRIDE = 16;
+constexpr int NCKPT = 16;
 
 // Per-rank accumulators shared by the rank's sub-banks (tasks).
 struct Acc {

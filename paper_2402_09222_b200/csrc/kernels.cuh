@@ -37,7 +37,7 @@ struct Ctx {
     unsigned long long* ctrl;  // [0] refill ticket, [1] alive, [2] error flags
 };
 
-constexpr int SMEM_TALLY_MAX = 2048;  // tally bins*scores aggregated per block in smem
+constexpr int SMEM_TALLY_MAX = 64;  // tally bins*scores aggregated per block in smem (few-pin problems)
 
 // bookkeeping
 void reset_launch_counter();
@@ -56,7 +56,9 @@ void launch_refill_all(const Ctx& c, int64_t first_local, int64_t n_remaining, c
 void launch_xs(const Ctx& c, const int32_t* q, int n, bool fuel, cudaStream_t s);
 void launch_advance(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 void launch_cross(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
-void launch_collide(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
+// the collision queue is double-ended: n_front fuel entries at the front,
+// n - n_front non-fuel entries at the back
+void launch_collide(const Ctx& c, const int32_t* q, int n, int n_front, cudaStream_t s);
 
 // material/energy sort of the fuel XS queue (16-bit energy radix per material)
 void launch_sort(const Ctx& c, const int32_t* q_in, int32_t* q_out, int n, int n_fuel_mats,

@@ -72,7 +72,7 @@ struct GpuProblem {
 
     void upload(const Problem& p, int n_bins, int device, cudaStream_t s) {
         arena.device = device;
-        if (n_bins < 1 || n_bins > 10000000) throw std::invalid_argument("n_bins (P2) out of range");
+        if (n_bins < 1 || n_bins > 1000000) throw std::invalid_argument("n_bins (P2) out of range [1, 1e6]");
         const int nn = p.n_nuc, nm = (int)p.mat.size();
         std::vector<int32_t> goff(nn + 1);
         for (int i = 0; i <= nn; ++i) goff[i] = (int32_t)p.goff[i];
@@ -92,6 +92,11 @@ struct GpuProblem {
         }
         moff[nm] = (int32_t)mnuc.size();
         n_fuel_mats = std::max(1, fuel_rank);
+        std::vector<int4> mdesc(mnuc.size());
+        for (size_t i = 0; i < mnuc.size(); ++i) {
+            int n = mnuc[i];
+            mdesc[i] = make_int4(goff[n], goff[n + 1] - goff[n], n * (n_bins + 1), n);
+        }
         auto up = [&](auto* dst, const auto* src, size_t n) {
             size_t bytes = sizeof(*src) * n;
             CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
@@ -103,6 +108,7 @@ struct GpuProblem {
         double* d_awr = arena.alloc<double>(nn);
         int32_t* d_moff = arena.alloc<int32_t>(nm + 1);
         int32_t* d_mnuc = arena.alloc<int32_t>((int64_t)mnuc.size());
+        int4* d_mdesc = arena.alloc<int4>((int64_t)mdesc.size());
         double* d_mdens = arena.alloc<double>((int64_t)mdens.size());
         uint8_t* d_mfis = arena.alloc<uint8_t>(nm);
         uint8_t* d_mfuel = arena.alloc<uint8_t>(nm);
@@ -115,6 +121,7 @@ struct GpuProblem {
         up(d_awr, p.awr.data(), p.awr.size());
         up(d_moff, moff.data(), moff.size());
         up(d_mnuc, mnuc.data(), mnuc.size());
+        up(d_mdesc, mdesc.data(), mdesc.size());
         up(d_mdens, mdens.data(), mdens.size());
         up(d_mfis, mfis.data(), mfis.size());
         up(d_mfuel, mfuel.data(), mfuel.size());
@@ -128,7 +135,7 @@ struct GpuProblem {
         lib.inv_spacing = (double)n_bins / ln_range;
         lib.log_emin = log_emin;
         lib.goff = d_goff; lib.E = d_E; lib.xs = d_xs; lib.hash = d_hash; lib.awr = d_awr;
-        lib.mat_off = d_moff; lib.mat_nuc = d_mnuc; lib.mat_dens = d_mdens;
+        lib.mat_off = d_moff; lib.mat_nuc = d_mnuc; lib.mat_desc = d_mdesc; lib.mat_dens = d_mdens;
         lib.mat_fissionable = d_mfis; lib.mat_fuel = d_mfuel; lib.mat_sort_rank = d_mrank;
         launch_hash_build(lib, d_hash, s);
         CK(cudaGetLastError());
@@ -264,6 +271,7 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         B.event = A.alloc<int8_t>(cap);
         B.n_xs = A.alloc<int32_t>(cap); B.n_adv = A.alloc<int32_t>(cap); B.n_cross = A.alloc<int32_t>(cap);
         B.n_coll = A.alloc<int32_t>(cap); B.n_sites = A.alloc<int32_t>(cap);
+        B.ckpt = A.alloc<double>((int64_t)NCKPT * cap);
         CK(cudaMemsetAsync(B.event, EV_DEAD, (size_t)cap, S.stream));
         S.qs.cap = cap;
         S.qs.qbase = A.alloc<int32_t>((int64_t)N_QUEUES * cap);
@@ -369,8 +377,12 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
             S.trace.back() = (int64_t)S.h_trace_chk[0];
             pending_trace = false;
         }
+        // queue lengths; the collision queue is double-ended (front count[4], back count[5])
+        int64_t qlen[EV_DEAD];
+        for (int k = 0; k < EV_DEAD; ++k) qlen[k] = S.h_counts[k];
+        qlen[EV_COLL] += S.h_counts[5];
         int64_t live = 0;
-        for (int k = 0; k < EV_DEAD; ++k) live += S.h_counts[k];
+        for (int k = 0; k < EV_DEAD; ++k) live += qlen[k];
         ull dead_tail;
         std::memcpy(&dead_tail, S.h_counts + 6, sizeof dead_tail);
         const int64_t dead = (int64_t)(dead_tail - S.dead_head);
@@ -383,8 +395,8 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
             }
             int best = 0;
             for (int k = 1; k < EV_DEAD; ++k)
-                if (S.h_counts[k] > S.h_counts[best]) best = k;
-            int n = (int)S.h_counts[best];
+                if (qlen[k] > qlen[best]) best = k;
+            int n = (int)qlen[best];
             if (next >= S.hi && live <= tail) {
                 // sparse end of the batch: one launch finishes every live history
                 best = EV_DEAD;
@@ -412,7 +424,10 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                 case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, false, S.stream); } break;
                 case EV_ADV: { Prof pf(S, prof, 2, n); launch_advance(c, qptr, n, S.stream); } break;
                 case EV_CROSS: { Prof pf(S, prof, 3, n); launch_cross(c, qptr, n, S.stream); } break;
-                default: { Prof pf(S, prof, 4, n); launch_collide(c, qptr, n, S.stream); } break;
+                default: {
+                    Prof pf(S, prof, 4, n);
+                    launch_collide(c, qptr, n, (int)S.h_counts[EV_COLL], S.stream);
+                } break;
                 }
             }
             c.trace_chk = nullptr;
@@ -446,7 +461,7 @@ void run_queueless(Rank& R, SubBank& S, Ctx c, const Site* src, bool prof, int64
         { Prof pf(S, prof, 0, S.b.cap); launch_xs(c, nullptr, 0, false, S.stream); }
         { Prof pf(S, prof, 2, S.b.cap); launch_advance(c, nullptr, 0, S.stream); }
         { Prof pf(S, prof, 3, S.b.cap); launch_cross(c, nullptr, 0, S.stream); }
-        { Prof pf(S, prof, 4, S.b.cap); launch_collide(c, nullptr, 0, S.stream); }
+        { Prof pf(S, prof, 4, S.b.cap); launch_collide(c, nullptr, 0, 0, S.stream); }
         CK(cudaMemcpyAsync(S.h_ctrl, S.ctrl, sizeof(ull) * 3, cudaMemcpyDeviceToHost, S.stream));
         CK(cudaStreamSynchronize(S.stream));
         if (prof) drain_profile(S);
