@@ -7,8 +7,7 @@ p = P.Problem("assembly")
 r = P.run(p, n_particles=1000000, n_batches=2, n_inactive=1).result
 print("FoM", r.fom)
 PY
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python /tmp/run2.py > gpurun_out/ncu_launch.log 2>&1; tail -2 gpurun_out/ncu_launch.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_xs_fuel -s 40 -c 1 -o gpurun_out/prof_xs_fuel python /tmp/run2.py > gpurun_out/ncu_xs.log 2>&1; tail -2 gpurun_out/ncu_xs.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_collide -s 40 -c 1 -o gpurun_out/prof_collide python /tmp/run2.py > gpurun_out/ncu_coll.log 2>&1; tail -2 gpurun_out/ncu_coll.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_advance -s 60 -c 1 -o gpurun_out/prof_advance python /tmp/run2.py > gpurun_out/ncu_adv.log 2>&1; tail -2 gpurun_out/ncu_adv.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_xs_fuel -s 40 -c 1 -o gpurun_out/prof_xs_fuel2 python /tmp/run2.py > gpurun_out/ncu_xs.log 2>&1; tail -2 gpurun_out/ncu_xs.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_collide -s 40 -c 1 -o gpurun_out/prof_collide2 python /tmp/run2.py > gpurun_out/ncu_coll.log 2>&1; tail -2 gpurun_out/ncu_coll.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_tail -s 1 -c 1 -o gpurun_out/prof_tail python /tmp/run2.py > gpurun_out/ncu_adv.log 2>&1; tail -2 gpurun_out/ncu_adv.log
 ls -la gpurun_out/
