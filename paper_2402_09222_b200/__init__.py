@@ -109,7 +109,11 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
                 trace_queues=False, tail_threshold=None) -> RunConfig:
     cfg = RunConfig()
     _lib.omcg_run_config_default(C.byref(cfg))
-    cfg.mode = QUEUELESS if mode in ("openmc-queueless", "queueless", QUEUELESS) else QUEUED
+    m = {"openmc": QUEUED, "queued": QUEUED, "openmc-queueless": QUEUELESS,
+         "queueless": QUEUELESS}.get(mode, mode) if isinstance(mode, str) else int(mode)
+    if isinstance(m, str):
+        raise ValueError(f"unknown mode {mode!r} (P0 is 'openmc' or 'openmc-queueless')")
+    cfg.mode = m
     cfg.particles_in_flight = int(particles_in_flight)
     cfg.n_bins = int(n_bins)
     cfg.sort_threshold = -1 if sort_threshold is None else int(sort_threshold)

@@ -19,7 +19,28 @@
 #include <thread>
 
 #include "kernels.cuh"
+#include "nccl_api.hpp"
 #include "transport.hpp"
+
+namespace omcg {
+inline NcclApi& nccl_checked() {
+    NcclApi& a = nccl();
+    if (!a.error.empty()) throw NcclError(a.error);
+    return a;
+}
+}  // namespace omcg
+// every NCCL call below goes through the dlopen'ed table
+#define ncclGetUniqueId omcg::nccl_checked().GetUniqueId
+#define ncclCommInitRank omcg::nccl_checked().CommInitRank
+#define ncclCommInitAll omcg::nccl_checked().CommInitAll
+#define ncclCommDestroy omcg::nccl_checked().CommDestroy
+#define ncclAllReduce omcg::nccl_checked().AllReduce
+#define ncclAllGather omcg::nccl_checked().AllGather
+#define ncclSend omcg::nccl_checked().Send
+#define ncclRecv omcg::nccl_checked().Recv
+#define ncclGroupStart omcg::nccl_checked().GroupStart
+#define ncclGroupEnd omcg::nccl_checked().GroupEnd
+#define ncclGetErrorString omcg::nccl_checked().GetErrorString
 
 namespace omcg {
 

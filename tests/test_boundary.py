@@ -1,0 +1,123 @@
+"""The process-level drop-in boundary: bin/openmc under the reference's own,
+unchanged tuner (oracle/_ref/libautotune.so built from /root/reference/proj/src)
+and unchanged campaign (proj/campaigns/openmc: space.json, openmc.sh.in,
+launcher.in, campaign.json; copied to oracle/_ref/campaigns by build_ref.sh).
+
+Pins: argv `--event -i P1 -b P2 [-m P3]`, mode from argv[0]
+(openmc / openmc-queueless), "FOM: <x> particles/s" on stdout (last match,
+proj/src/harness.cpp:150-171), metrics.txt "<package_J> <dram_J>"
+(harness.cpp:117-136), nonzero exit -> status fail + penalty (harness.cpp:292).
+"""
+import csv
+import json
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "bin")
+REF = os.path.join(ROOT, "oracle", "_ref")
+CAMPAIGN = os.path.join(REF, "campaigns", "openmc", "campaign.json")
+have_ref = pytest.mark.skipif(not os.path.exists(os.path.join(REF, "atune_run")),
+                              reason="reference tuner not built (oracle/build_ref.sh needs /root/reference)")
+
+
+def has_gpu():
+    from conftest import _has_gpu
+    return _has_gpu()
+
+
+def run_openmc(args, env=None, cwd=None, name="openmc"):
+    e = dict(os.environ)
+    e.update(env or {})
+    return subprocess.run([os.path.join(BIN, name)] + args, capture_output=True, text=True, env=e, cwd=cwd,
+                          timeout=600)
+
+
+def test_usage_errors_exit_2(tmp_path):
+    assert run_openmc(["--event", "-i"], cwd=tmp_path).returncode == 2
+    assert run_openmc(["--event", "-q", "5"], cwd=tmp_path).returncode == 2
+    r = run_openmc(["-i", "100", "-b", "100"], cwd=tmp_path)
+    assert r.returncode == 2 and "--event" in r.stderr
+
+
+@pytest.mark.skipif(has_gpu(), reason="GPU visible")
+def test_no_gpu_fails_loudly(tmp_path):
+    r = run_openmc(["--event", "-i", "1000", "-b", "100", "-m", "0"], cwd=tmp_path)
+    assert r.returncode == 3
+    assert "CUDA" in r.stderr or "cuda" in r.stderr
+    assert "FOM" not in r.stdout
+
+
+def read_results(path):
+    with open(path) as f:
+        return list(csv.DictReader(f))
+
+
+def run_campaign(campaign, out, evals, workers, env):
+    e = dict(os.environ)
+    e["PATH"] = BIN + os.pathsep + e["PATH"]
+    e.update(env)
+    r = subprocess.run([os.path.join(REF, "atune_run"), campaign, str(out), str(evals), str(workers)],
+                       capture_output=True, text=True, env=e, timeout=1800)
+    return r, read_results(os.path.join(out, "results.csv"))
+
+
+@have_ref
+@pytest.mark.skipif(has_gpu(), reason="GPU visible")
+def test_reference_harness_records_failures_without_gpu(tmp_path):
+    r, rows = run_campaign(CAMPAIGN, tmp_path / "run", 3, 2, {})
+    assert len(rows) == 3
+    assert all(row["status"] == "fail" and float(row["objective"]) == -1.0 for row in rows)
+    # the unchanged mold called our binary with the documented argv
+    script = open(tmp_path / "run" / "evals" / "0" / "script").read()
+    assert "openmc --event -i" in script or "openmc-queueless --event -i" in script
+
+
+SMALL = {"OMCG_PARTICLES": "20000", "OMCG_BATCHES": "3", "OMCG_INACTIVE": "1", "OMCG_LEASE_DIR": "/tmp"}
+
+
+@pytest.mark.gpu
+def test_openmc_binary_contract(tmp_path):
+    for name, args in (("openmc", ["--event", "-i", "20000", "-b", "4000", "-m", "20000"]),
+                       ("openmc-queueless", ["--event", "-i", "20000", "-b", "4000"]),
+                       ("openmc", ["--event", "-i", "5000", "-b", "100", "-m", "nan"])):
+        d = tmp_path / name / args[2]
+        d.mkdir(parents=True)
+        r = run_openmc(args, env=dict(SMALL, AUTOTUNE_LAUNCHER_ARGS="-c 4 --ntasks-per-gpu=2 --cpu-bind=cores"),
+                       cwd=d, name=name)
+        assert r.returncode == 0, r.stderr
+        fom = [l for l in r.stdout.splitlines() if l.startswith("FOM:")]
+        assert len(fom) == 1 and fom[0].endswith("particles/s") and float(fom[0].split()[1]) > 0
+        pkg, dram = open(d / "metrics.txt").read().split()
+        assert float(pkg) >= 0 and float(dram) >= 0
+        assert ("queueless" in r.stderr) == (name == "openmc-queueless")
+        assert "P5=2" in r.stderr and "P4=4" in r.stderr
+
+
+@have_ref
+@pytest.mark.gpu
+def test_unchanged_reference_campaign_runs_on_gpu_fom(tmp_path):
+    r, rows = run_campaign(CAMPAIGN, tmp_path / "fom", 6, 2, SMALL)
+    assert r.returncode == 0, r.stderr
+    assert len(rows) == 6 and all(row["status"] == "ok" for row in rows), rows
+    for row in rows:
+        out = open(tmp_path / "fom" / "evals" / row["eval_id"] / "stdout.log").read()
+        last = [l for l in out.splitlines() if l.startswith("FOM:")][-1]
+        assert float(row["objective"]) == pytest.approx(float(last.split()[1]), rel=1e-9)
+
+
+@have_ref
+@pytest.mark.gpu
+def test_unchanged_reference_campaign_runs_on_gpu_edp(tmp_path):
+    src = json.load(open(CAMPAIGN))
+    d = os.path.dirname(CAMPAIGN)
+    src.update(space_file=os.path.join(d, src["space_file"]), mold_file=os.path.join(d, src["mold_file"]),
+               launcher_file=os.path.join(d, src["launcher_file"]), metric={"kind": "edp"})
+    src.pop("baseline", None)
+    cj = tmp_path / "edp_campaign.json"
+    cj.write_text(json.dumps(src))
+    r, rows = run_campaign(str(cj), tmp_path / "edp", 4, 2, SMALL)
+    assert r.returncode == 0, r.stderr
+    assert all(row["status"] == "ok" and float(row["objective"]) > 0 for row in rows), rows
