@@ -90,7 +90,7 @@ typedef struct {
     /* diagnostics */
     int record_batch;             /* 1-based batch whose first record_n histories are recorded */
     int64_t record_n;
-    int profile;                  /* time every kernel class with CUDA events */
+    int profile;                  /* CUDA-event timing: 1 every kernel class, 2 fuel calculate_xs only */
     int trace_queues;             /* record per-iteration (queue, length, id-checksum) */
     /* When the source is exhausted and at most tail_threshold histories are
      * alive, finish them in one history-per-thread launch instead of one

@@ -134,7 +134,7 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
         C.memmove(cfg.nccl_id, nccl_id, 128)
     cfg.record_batch = int(record_batch)
     cfg.record_n = int(record_n)
-    cfg.profile = int(bool(profile))
+    cfg.profile = int(profile)  # True/1: every kernel class; 2: fuel calculate_xs only
     cfg.trace_queues = int(bool(trace_queues))
     if tail_threshold is not None:
         cfg.tail_threshold = int(tail_threshold)

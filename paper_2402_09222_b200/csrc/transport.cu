@@ -182,6 +182,7 @@ struct SubBank {
     ull* h_trace_chk = nullptr;
     int64_t lo = 0, hi = 0;        // rank-local history range
     int64_t tail_launches = 0;
+    int prof_level = 0;
     std::vector<int64_t> trace;
     // profile
     struct EvPair {
@@ -279,6 +280,7 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         int64_t cap = std::min<int64_t>(std::max<int64_t>(cfg.particles_in_flight, 1), std::max<int64_t>(S.hi - S.lo, 1));
         if (cap > (int64_t)1 << 30) throw std::invalid_argument("particles in flight too large");
         S.b.cap = cap;
+        S.prof_level = cfg.profile;
         CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
         Bank& B = S.b;
         B.x = A.alloc<double>(cap); B.y = A.alloc<double>(cap); B.z = A.alloc<double>(cap);
@@ -369,7 +371,9 @@ void drain_profile(SubBank& S) {
 struct Prof {
     SubBank& S;
     bool on;
-    Prof(SubBank& s, bool enabled, int cls, int64_t items) : S(s), on(enabled) {
+    // profile level 1 times every kernel class; level 2 only the fuel calculate_xs
+    Prof(SubBank& s, bool enabled, int cls, int64_t items)
+        : S(s), on(enabled && (S.prof_level == 1 || cls == 0)) {
         if (!on) return;
         if (S.n_pending == (int)S.evs.size()) drain_profile(S);
         auto& e = S.evs[S.n_pending];
