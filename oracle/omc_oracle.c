@@ -679,22 +679,30 @@ static inline double interp(const double* xs, int i, int c, double f) {
     return a + f * (b - a);
 }
 
+/* Macroscopic sums are segmented: the material's nuclides (in material order)
+ * form segments of SEG_LEN; each segment is summed sequentially from 0 and the
+ * segment sums are folded in order into the total. (Segments are independent
+ * units of work for the GPU; for materials of <= SEG_LEN nuclides this is the
+ * plain sequential sum.) */
+#define SEG_LEN 16
 static void macro_xs(const orc_problem* p, int m, double E, double out[4]) {
     const material* M = &p->mat[m];
     int b = bin_of(p, E);
-    double t = 0.0, a = 0.0, fi = 0.0, nf = 0.0;
-    for (int q = 0; q < M->n; ++q) {
-        int n = M->nuc[q];
-        double f;
-        int i = grid_index(p, n, E, b, &f);
-        const double* xs = p->nuc[n].xs;
-        double d = M->dens[q];
-        t = t + d * interp(xs, i, 0, f);
-        a = a + d * interp(xs, i, 1, f);
-        fi = fi + d * interp(xs, i, 2, f);
-        nf = nf + d * interp(xs, i, 3, f);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int s0 = 0; s0 < M->n; s0 += SEG_LEN) {
+        double seg[4] = {0.0, 0.0, 0.0, 0.0};
+        int s1 = s0 + SEG_LEN < M->n ? s0 + SEG_LEN : M->n;
+        for (int q = s0; q < s1; ++q) {
+            int n = M->nuc[q];
+            double f;
+            int i = grid_index(p, n, E, b, &f);
+            const double* xs = p->nuc[n].xs;
+            double d = M->dens[q];
+            for (int c = 0; c < 4; ++c) seg[c] = seg[c] + d * interp(xs, i, c, f);
+        }
+        for (int c = 0; c < 4; ++c) acc[c] = acc[c] + seg[c];
     }
-    out[0] = t; out[1] = a; out[2] = fi; out[3] = nf;
+    for (int c = 0; c < 4; ++c) out[c] = acc[c];
 }
 
 int orc_hash_bin(const orc_problem* p, double E) { return bin_of(p, E); }
@@ -993,16 +1001,23 @@ static int ev_collide(const orc_problem* p, particle* q, accum* A, double k_norm
     q->n_coll++;
     const material* M = &p->mat[q->mat];
     int b = bin_of(p, q->E);
-    /* sample the target nuclide from cumulative rho_n sigma_t,n */
+    /* sample the target nuclide from the cumulative rho_n sigma_t,n, accumulated
+     * with the same segmented sums as macro_xs: cum = (folded earlier segments)
+     * + (running sum inside the current segment) */
     double cutoff = orc_prn(&q->seed) * q->st;
-    double cum = 0.0;
-    int sel = M->n - 1;
-    for (int j = 0; j < M->n; ++j) {
-        double f;
-        int n = M->nuc[j];
-        int i = grid_index(p, n, q->E, b, &f);
-        cum = cum + M->dens[j] * interp(p->nuc[n].xs, i, 0, f);
-        if (cum > cutoff) { sel = j; break; }
+    double acc = 0.0;
+    int sel = M->n - 1, found = 0;
+    for (int s0 = 0; s0 < M->n && !found; s0 += SEG_LEN) {
+        int s1 = s0 + SEG_LEN < M->n ? s0 + SEG_LEN : M->n;
+        double seg = 0.0;
+        for (int j = s0; j < s1; ++j) {
+            double f;
+            int n = M->nuc[j];
+            int i = grid_index(p, n, q->E, b, &f);
+            seg = seg + M->dens[j] * interp(p->nuc[n].xs, i, 0, f);
+            if (acc + seg > cutoff) { sel = j; found = 1; break; }
+        }
+        acc = acc + seg;
     }
     int n = M->nuc[sel];
     double f;

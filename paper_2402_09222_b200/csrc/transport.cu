@@ -89,6 +89,7 @@ struct GpuProblem {
     DevLib lib{};
     Geometry geo{};
     int n_fuel_mats = 0;
+    int max_fuel_seg = 1;  // 16-nuclide segments of the largest fuel-queue material
     int64_t h2d_bytes = 0;
 
     void upload(const Problem& p, int n_bins, int device, cudaStream_t s) {
@@ -113,6 +114,9 @@ struct GpuProblem {
         }
         moff[nm] = (int32_t)mnuc.size();
         n_fuel_mats = std::max(1, fuel_rank);
+        for (int m = 0; m < nm; ++m)
+            if (mfuel[m])
+                max_fuel_seg = std::max(max_fuel_seg, (int)((p.mat[m].nuc.size() + CKPT_STRIDE - 1) / CKPT_STRIDE));
         std::vector<int4> mdesc(mnuc.size());
         for (size_t i = 0; i < mnuc.size(); ++i) {
             int n = mnuc[i];
@@ -170,6 +174,7 @@ struct SubBank {
     Bank b{};
     QueueSet qs{};
     int32_t* q_sorted = nullptr;
+    double* part = nullptr;  // split fuel calculate_xs partial sums [seg][4][cap]
     uint32_t* keys = nullptr;
     unsigned* hist = nullptr;
     unsigned* cursor = nullptr;
@@ -312,6 +317,7 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
             S.dead_head = 0;
         }
         S.q_sorted = A.alloc<int32_t>(cap);
+        S.part = A.alloc<double>((int64_t)R.gp.max_fuel_seg * 4 * cap);
         S.keys = A.alloc<uint32_t>(cap);
         S.hist = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
         S.cursor = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
@@ -352,6 +358,15 @@ void teardown_rank(Rank& R) {
 }
 
 // ------------------------------------------------------------------ event loops
+// OMCG_XS_SPLIT=0 selects the one-history-per-thread fuel lookup (A/B switch)
+bool xs_split() {
+    static const bool on = [] {
+        const char* v = std::getenv("OMCG_XS_SPLIT");
+        return !v || std::atoi(v) != 0;
+    }();
+    return on;
+}
+
 // Per-kernel CUDA-event timing on the launching stream. Events are recorded
 // around each launch and read back only after the loop's next host sync, so
 // profiling adds two event records per launch and no extra synchronisation.
@@ -442,7 +457,8 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                     }
                     {
                         Prof pf(S, prof, 0, n);
-                        launch_xs(c, qptr, n, true, S.stream);
+                        if (xs_split()) launch_xs_fuel_split(c, qptr, n, R.gp.max_fuel_seg, S.part, S.stream);
+                        else launch_xs(c, qptr, n, true, S.stream);
                     }
                     if (prof) S.xs_fuel_bytes += (double)n * (44.0 + 100.0 * (double)fuel_nuc);
                     break;
