@@ -39,14 +39,30 @@ struct Site {
     uint64_t key;  // (batch-global history index << 24) | progeny
 };
 
+// Hot per-history state: one 128-byte record per in-flight slot. The event
+// kernels reach a history through a queue entry (a gather), so what costs is
+// the number of distinct 32 B sectors touched per event: a record keeps every
+// field an event needs in one 128 B line (4 sectors, 16 B vector loads)
+// instead of ~16 scattered SoA sectors.
+struct alignas(128) PState {
+    double x, y, z;         // position (cm)
+    double u, v, w;         // direction
+    double E, wgt;          // energy (eV), weight
+    double st, sa, sf, snf; // macroscopic total / absorption / fission / nu-fission (1/cm)
+    uint64_t seed;          // RNG state
+    int32_t cell;           // global pin index gy*nx + gx
+    int32_t gidx;           // batch-global history index
+    int8_t ring, mat, surf, pad0;
+    int32_t n_sites;        // fission sites banked so far
+    int32_t pad1[2];
+};
+static_assert(sizeof(PState) == 128, "PState must be one 128-byte line");
+
 struct Bank {
     int64_t cap;
-    double *x, *y, *z, *u, *v, *w, *E, *wgt;
-    double *st, *sa, *sf, *snf;
-    uint64_t* seed;
-    int32_t *gidx, *cell;
-    int8_t *ring, *mat, *surf, *event;
-    int32_t *n_xs, *n_adv, *n_cross, *n_coll, *n_sites;
+    PState* p;         // cap records
+    int4* cnt;         // per-slot event counters: n_xs, n_adv, n_cross, n_coll
+    int8_t* event;     // dense next-event array (queueless sweeps, tail, refill)
     // running macroscopic total after every CKPT_STRIDE nuclides of a large
     // material (written by calculate_xs, read by collision to jump straight
     // to the segment holding the sampled nuclide): NCKPT x cap

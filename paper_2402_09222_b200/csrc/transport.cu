@@ -288,17 +288,9 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         S.prof_level = cfg.profile;
         CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
         Bank& B = S.b;
-        B.x = A.alloc<double>(cap); B.y = A.alloc<double>(cap); B.z = A.alloc<double>(cap);
-        B.u = A.alloc<double>(cap); B.v = A.alloc<double>(cap); B.w = A.alloc<double>(cap);
-        B.E = A.alloc<double>(cap); B.wgt = A.alloc<double>(cap);
-        B.st = A.alloc<double>(cap); B.sa = A.alloc<double>(cap); B.sf = A.alloc<double>(cap);
-        B.snf = A.alloc<double>(cap);
-        B.seed = A.alloc<uint64_t>(cap);
-        B.gidx = A.alloc<int32_t>(cap); B.cell = A.alloc<int32_t>(cap);
-        B.ring = A.alloc<int8_t>(cap); B.mat = A.alloc<int8_t>(cap); B.surf = A.alloc<int8_t>(cap);
+        B.p = A.alloc<PState>(cap);
+        B.cnt = A.alloc<int4>(cap);
         B.event = A.alloc<int8_t>(cap);
-        B.n_xs = A.alloc<int32_t>(cap); B.n_adv = A.alloc<int32_t>(cap); B.n_cross = A.alloc<int32_t>(cap);
-        B.n_coll = A.alloc<int32_t>(cap); B.n_sites = A.alloc<int32_t>(cap);
         B.ckpt = A.alloc<double>((int64_t)NCKPT * cap);
         CK(cudaMemsetAsync(B.event, EV_DEAD, (size_t)cap, S.stream));
         S.qs.cap = cap;
