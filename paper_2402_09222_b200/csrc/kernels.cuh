@@ -50,7 +50,9 @@ void launch_xs_pairs(const DevLib& lib, int64_t n, const int32_t* mat, const dou
 
 // event kernels; q == nullptr selects the queueless variant over all cap slots
 void launch_init(const Ctx& c, uint64_t head, int n, int64_t first_local, const Site* src, cudaStream_t s);
-void launch_tail(const Ctx& c, bool queued, cudaStream_t s);
+// list != nullptr: warp-per-history tail over the `live` remaining histories
+// (ctrl[3] must be zero); nullptr: thread-per-slot tail
+void launch_tail(const Ctx& c, bool queued, int64_t live, int32_t* list, cudaStream_t s);
 void launch_refill_all(const Ctx& c, int64_t first_local, int64_t n_remaining, const Site* src,
                        cudaStream_t s);
 void launch_xs(const Ctx& c, const int32_t* q, int n, bool fuel, cudaStream_t s);

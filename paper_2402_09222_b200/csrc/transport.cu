@@ -175,6 +175,7 @@ struct SubBank {
     QueueSet qs{};
     int32_t* q_sorted = nullptr;
     double* part = nullptr;  // split fuel calculate_xs partial sums [seg][4][cap]
+    int32_t* tail_list = nullptr;  // live slots for the warp-per-history tail
     uint32_t* keys = nullptr;
     unsigned* hist = nullptr;
     unsigned* cursor = nullptr;
@@ -310,6 +311,7 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         }
         S.q_sorted = A.alloc<int32_t>(cap);
         S.part = A.alloc<double>((int64_t)R.gp.max_fuel_seg * 4 * cap);
+        S.tail_list = A.alloc<int32_t>(cap);
         S.keys = A.alloc<uint32_t>(cap);
         S.hist = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
         S.cursor = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
@@ -350,12 +352,18 @@ void teardown_rank(Rank& R) {
 }
 
 // ------------------------------------------------------------------ event loops
-// OMCG_XS_SPLIT=0 selects the one-history-per-thread fuel lookup (A/B switch)
+// A/B switches: OMCG_XS_SPLIT=0 selects the one-history-per-thread fuel
+// lookup, OMCG_TAIL_WARP=0 the thread-per-history tail.
+bool env_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return !v || std::atoi(v) != 0;
+}
 bool xs_split() {
-    static const bool on = [] {
-        const char* v = std::getenv("OMCG_XS_SPLIT");
-        return !v || std::atoi(v) != 0;
-    }();
+    static const bool on = env_flag("OMCG_XS_SPLIT");
+    return on;
+}
+bool tail_warp() {
+    static const bool on = env_flag("OMCG_TAIL_WARP");
     return on;
 }
 
@@ -433,8 +441,9 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                 // sparse end of the batch: one launch finishes every live history
                 best = EV_DEAD;
                 n = (int)live;
+                CK(cudaMemsetAsync(S.ctrl + 3, 0, sizeof(ull), S.stream));
                 Prof pf(S, prof, 7, live);
-                launch_tail(c, true, S.stream);
+                launch_tail(c, true, live, tail_warp() ? S.tail_list : nullptr, S.stream);
                 S.tail_launches++;
             } else {
                 const int32_t* qptr = S.qs.qbase + (int64_t)best * S.qs.cap;
@@ -503,8 +512,9 @@ void run_queueless(Rank& R, SubBank& S, Ctx c, const Site* src, bool prof, int64
         const int64_t alive = (int64_t)S.h_ctrl[1];
         if (alive == 0 && next >= S.hi) break;
         if (next >= S.hi && alive <= tail) {
+            CK(cudaMemsetAsync(S.ctrl + 3, 0, sizeof(ull), S.stream));
             Prof pf(S, prof, 7, alive);
-            launch_tail(c, false, S.stream);
+            launch_tail(c, false, alive, tail_warp() ? S.tail_list : nullptr, S.stream);
             S.tail_launches++;
             CK(cudaStreamSynchronize(S.stream));
             break;

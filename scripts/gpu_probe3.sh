@@ -10,5 +10,5 @@ for prof in (0, 1):
     print(f"$1 prof={prof} FoM={r.fom:.4e} t_active={r.t_active:.3f} k={r.k_mean:.6f}", " ".join(f"{n}={r.prof_ms[i]/5:.1f}ms" for i,n in enumerate(names)) if prof else "")
 PY
 }
-OMCG_XS_SPLIT=0 run single
-OMCG_XS_SPLIT=1 run split
+OMCG_TAIL_WARP=0 run tail_thread
+OMCG_TAIL_WARP=1 run tail_warp
