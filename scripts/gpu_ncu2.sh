@@ -1,0 +1,11 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
+python scripts/../scripts/run_c2.py 7 2
+cat > /tmp/run2.py <<'PY'
+import sys; sys.path.insert(0,'.')
+import paper_2402_09222_b200 as P
+p = P.Problem("assembly")
+r = P.run(p, n_particles=1000000, n_batches=2, n_inactive=1).result
+print("FoM", r.fom)
+PY
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^k_xs_fuel_seg$" -s 30 -c 1 -o gpurun_out/r01b_k_xs_fuel_seg python /tmp/run2.py > gpurun_out/ncu_seg.log 2>&1; tail -1 gpurun_out/ncu_seg.log
