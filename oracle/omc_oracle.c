@@ -1095,6 +1095,94 @@ static void transport(const orc_problem* p, particle* q, accum* A, double k_norm
 }
 
 /* ------------------------------------------------------------------ */
+/* queued event-loop emulation (queue contents)          */
+/* ------------------------------------------------------------------ */
+/* Restates the queued scheduling policy of the product's event loop so the
+ * per-iteration queue contents can be compared: an in-flight bank of P1 slots;
+ * each iteration reads the queue lengths, runs every particle of the longest
+ * queue (ties: fuel XS, non-fuel XS, advance, crossing, collision) and then
+ * refills the slots that were empty at the start of the iteration from the
+ * source; once the source is exhausted and at most
+ * tail_threshold histories are alive, all of them are finished at once
+ * (recorded as queue 5). Trace entries: (queue, length, sum of mix64(id+1)). */
+enum { Q_XS_FUEL = 0, Q_XS_NONFUEL = 1, Q_ADV = 2, Q_CROSS = 3, Q_COLL = 4, Q_DEAD = 5 };
+
+static uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, int64_t in_flight,
+                    int64_t tail_threshold, int64_t* out, int64_t max_entries, int64_t* n_out) {
+    if (!p || !n_out || n_particles < 1 || in_flight < 1) return fail("invalid queue-trace arguments");
+    int64_t cap = in_flight < n_particles ? in_flight : n_particles;
+    particle* slots = (particle*)malloc(sizeof(particle) * (size_t)cap);
+    int* ev = (int*)malloc(sizeof(int) * (size_t)cap);
+    accum A;
+    memset(&A, 0, sizeof A);
+    A.tally = (int64_t*)calloc(4 * (size_t)p->geo.nx * (size_t)p->geo.ny, sizeof(int64_t));
+    if (!slots || !ev || !A.tally) {
+        free(slots); free(ev); free(A.tally);
+        return fail("out of memory");
+    }
+    for (int64_t s = 0; s < cap; ++s) ev[s] = Q_DEAD;
+    int64_t next = 0, n = 0;
+    int rc = 0;
+    for (;;) {
+        int64_t len[6] = {0, 0, 0, 0, 0, 0};
+        for (int64_t s = 0; s < cap; ++s) len[ev[s]]++;
+        int64_t live = len[0] + len[1] + len[2] + len[3] + len[4];
+        int64_t dead = len[Q_DEAD];
+        if (live == 0 && next >= n_particles) break;
+        if (live > 0) {
+            int best = 0;
+            for (int k = 1; k < 5; ++k)
+                if (len[k] > len[best]) best = k;
+            int tail = next >= n_particles && live <= tail_threshold;
+            uint64_t chk = 0;
+            for (int64_t s = 0; s < cap; ++s) {
+                if (ev[s] == Q_DEAD || (!tail && ev[s] != best)) continue;
+                particle* q = &slots[s];
+                chk += mix64((uint64_t)q->gidx + 1ULL);
+                int e = ev[s] <= Q_XS_NONFUEL ? EV_XS : ev[s] == Q_ADV ? EV_ADV : ev[s] == Q_CROSS ? EV_CROSS : EV_COLL;
+                do {  /* one event, or the whole remainder in the tail */
+                    switch (e) {
+                    case EV_XS: e = ev_xs(p, q); break;
+                    case EV_ADV: e = ev_advance(p, q, &A); break;
+                    case EV_CROSS: e = ev_cross(p, q); break;
+                    default: e = ev_collide(p, q, &A, 1.0); break;
+                    }
+                } while (tail && e != EV_DEAD);
+                ev[s] = e == EV_DEAD ? Q_DEAD : e == EV_XS ? (p->mat[q->mat].fissionable ? Q_XS_FUEL : Q_XS_NONFUEL)
+                        : e == EV_ADV ? Q_ADV : e == EV_CROSS ? Q_CROSS : Q_COLL;
+            }
+            if (out && n < max_entries) {
+                out[3 * n] = tail ? Q_DEAD : best;
+                out[3 * n + 1] = tail ? live : len[best];
+                out[3 * n + 2] = (int64_t)chk;
+            }
+            n++;
+        }
+        /* refill slots that were empty when the iteration started */
+        if (dead > 0 && next < n_particles) {
+            int64_t k = dead < n_particles - next ? dead : n_particles - next;
+            for (int64_t s = 0; s < cap && k > 0; ++s) {
+                if (ev[s] != Q_DEAD) continue;
+                if (init_particle(p, &slots[s], seed, 1, n_particles, next, NULL) != 0) { rc = -1; break; }
+                ev[s] = p->mat[slots[s].mat].fissionable ? Q_XS_FUEL : Q_XS_NONFUEL;
+                next++;
+                k--;
+            }
+            if (rc) break;
+        }
+    }
+    *n_out = n;
+    free(slots); free(ev); free(A.tally); free(A.bank);
+    return rc;
+}
+
+/* ------------------------------------------------------------------ */
 /* batch driver (threaded over histories)                              */
 /* ------------------------------------------------------------------ */
 typedef struct {
