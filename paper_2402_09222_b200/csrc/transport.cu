@@ -15,6 +15,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <condition_variable>
+#include <memory>
 #include <mutex>
 #include <thread>
 
@@ -236,14 +238,13 @@ struct SubBank {
     int64_t iterations = 0, sorts = 0;
 };
 
-struct RankShared {
-    // collective results of all ranks (max over ranks etc.)
-    std::mutex mu;
-};
+struct BatchComm;
 
 struct Rank {
     int device = 0, rank = 0, world = 1;
     ncclComm_t comm = nullptr;
+    BatchComm* bc = nullptr;          // per-batch collectives (NCCL or in-process loopback)
+    std::vector<ull> sall;            // bank sizes of all ranks, this batch
     DevArena arena;
     GpuProblem gp;
     Acc acc{};
@@ -554,6 +555,137 @@ void run_queueless(Rank& R, SubBank& S, Ctx c, const Site* src, bool prof, int64
     }
 }
 
+// ------------------------------------------------------------------ collectives
+// The three per-batch exchanges of the multi-rank path:
+// exact int64 sums of k/counters/tallies + all-gather of bank sizes; the
+// canonical fission-bank slices of bank_exchange_plan; max of the timed region.
+struct BatchComm {
+    virtual ~BatchComm() = default;
+    virtual void reduce_batch(Rank& R, bool active) = 0;  // fills R.sall
+    virtual void exchange(Rank& R, const int64_t* plan) = 0;
+    virtual double max_over_ranks(Rank& R, double v) = 0;
+};
+
+// NCCL over NVLink between ranks on different GPUs.
+struct NcclBatchComm : BatchComm {
+    void reduce_batch(Rank& R, bool active) override {
+        NK(ncclGroupStart());
+        NK(ncclAllReduce(R.acc.k, R.acc.k, 3, ncclUint64, ncclSum, R.comm, R.main));
+        NK(ncclAllReduce(R.acc.counts, R.acc.counts, 8, ncclUint64, ncclSum, R.comm, R.main));
+        if (active)
+            NK(ncclAllReduce(R.acc.tally, R.acc.tally, 4 * (size_t)R.n_tally_bins, ncclUint64, ncclSum, R.comm,
+                             R.main));
+        NK(ncclAllGather(R.acc.bank_count, R.d_sall, 1, ncclUint64, R.comm, R.main));
+        NK(ncclGroupEnd());
+        R.sall.resize(R.world);
+        CK(cudaMemcpyAsync(R.sall.data(), R.d_sall, sizeof(ull) * R.world, cudaMemcpyDeviceToHost, R.main));
+        CK(cudaStreamSynchronize(R.main));
+    }
+    void exchange(Rank& R, const int64_t* plan) override {
+        const int W = R.world;
+        NK(ncclGroupStart());
+        for (int r = 0; r < W; ++r) {
+            int64_t sf = plan[r], sc = plan[W + r], rf = plan[2 * W + r], rc = plan[3 * W + r];
+            if (r == R.rank) {
+                if (sc > 0)
+                    CK(cudaMemcpyAsync(R.recv + rf, R.canon + sf, sizeof(Site) * (size_t)sc, cudaMemcpyDeviceToDevice,
+                                       R.main));
+                continue;
+            }
+            if (sc > 0) NK(ncclSend(R.canon + sf, sizeof(Site) * (size_t)sc, ncclChar, r, R.comm, R.main));
+            if (rc > 0) NK(ncclRecv(R.recv + rf, sizeof(Site) * (size_t)rc, ncclChar, r, R.comm, R.main));
+        }
+        NK(ncclGroupEnd());
+    }
+    double max_over_ranks(Rank& R, double v) override {
+        CK(cudaMemcpyAsync(R.d_time, &v, sizeof(double), cudaMemcpyHostToDevice, R.main));
+        NK(ncclAllReduce(R.d_time, R.d_time, 1, ncclFloat64, ncclMax, R.comm, R.main));
+        CK(cudaMemcpyAsync(&v, R.d_time, sizeof(double), cudaMemcpyDeviceToHost, R.main));
+        CK(cudaStreamSynchronize(R.main));
+        return v;
+    }
+};
+
+// In-process loopback for ranks that share one GPU (devices[] with repeats):
+// the same exchanges through host staging and device-to-device pulls, so the
+// multi-rank path (partition, reductions, bank redistribution) runs and is
+// tested on a single B200.
+struct LoopbackShared {
+    int world = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int count = 0;
+    uint64_t gen = 0;
+    std::vector<std::vector<ull>> host;
+    std::vector<Site*> canon;
+    std::vector<double> vals;
+    explicit LoopbackShared(int w) : world(w), host(w), canon(w), vals(w) {}
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const uint64_t g = gen;
+        if (++count == world) {
+            count = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+
+struct LoopbackBatchComm : BatchComm {
+    LoopbackShared* sh;
+    explicit LoopbackBatchComm(LoopbackShared* s) : sh(s) {}
+    void reduce_batch(Rank& R, bool active) override {
+        const size_t nt = active ? 4 * (size_t)R.n_tally_bins : 0;
+        std::vector<ull>& h = sh->host[R.rank];
+        h.assign(3 + 8 + nt + 1, 0);
+        CK(cudaMemcpyAsync(h.data(), R.acc.k, sizeof(ull) * 3, cudaMemcpyDeviceToHost, R.main));
+        CK(cudaMemcpyAsync(h.data() + 3, R.acc.counts, sizeof(ull) * 8, cudaMemcpyDeviceToHost, R.main));
+        if (nt) CK(cudaMemcpyAsync(h.data() + 11, R.acc.tally, sizeof(ull) * nt, cudaMemcpyDeviceToHost, R.main));
+        CK(cudaMemcpyAsync(h.data() + 11 + nt, R.acc.bank_count, sizeof(ull), cudaMemcpyDeviceToHost, R.main));
+        CK(cudaStreamSynchronize(R.main));
+        sh->barrier();
+        std::vector<ull> sum(11 + nt, 0);
+        R.sall.assign(R.world, 0);
+        for (int r = 0; r < R.world; ++r) {
+            for (size_t i = 0; i < sum.size(); ++i) sum[i] += sh->host[r][i];
+            R.sall[r] = sh->host[r][11 + nt];
+        }
+        sh->barrier();  // every rank has read the staging before it is reused
+        CK(cudaMemcpyAsync(R.acc.k, sum.data(), sizeof(ull) * 3, cudaMemcpyHostToDevice, R.main));
+        CK(cudaMemcpyAsync(R.acc.counts, sum.data() + 3, sizeof(ull) * 8, cudaMemcpyHostToDevice, R.main));
+        if (nt) CK(cudaMemcpyAsync(R.acc.tally, sum.data() + 11, sizeof(ull) * nt, cudaMemcpyHostToDevice, R.main));
+        CK(cudaMemcpyAsync(R.d_sall, R.sall.data(), sizeof(ull) * R.world, cudaMemcpyHostToDevice, R.main));
+        CK(cudaStreamSynchronize(R.main));
+    }
+    void exchange(Rank& R, const int64_t* plan) override {
+        const int W = R.world;
+        CK(cudaStreamSynchronize(R.main));  // canonical bank complete
+        sh->canon[R.rank] = R.canon;
+        sh->barrier();
+        std::vector<uint64_t> G(W + 1, 0);
+        for (int r = 0; r < W; ++r) G[r + 1] = G[r] + R.sall[r];
+        const uint64_t my_a = (uint64_t)plan[4 * W];
+        for (int r = 0; r < W; ++r) {
+            const int64_t rf = plan[2 * W + r], rc = plan[3 * W + r];
+            if (rc > 0)
+                CK(cudaMemcpyAsync(R.recv + rf, sh->canon[r] + (my_a + (uint64_t)rf - G[r]), sizeof(Site) * (size_t)rc,
+                                   cudaMemcpyDeviceToDevice, R.main));
+        }
+        CK(cudaStreamSynchronize(R.main));
+        sh->barrier();  // all pulls done before any rank rewrites its canonical bank
+    }
+    double max_over_ranks(Rank& R, double v) override {
+        sh->vals[R.rank] = v;
+        sh->barrier();
+        double m = v;
+        for (double x : sh->vals) m = std::max(m, x);
+        sh->barrier();
+        return m;
+    }
+};
+
 // ------------------------------------------------------------------ batches
 void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     CK(cudaSetDevice(R.device));
@@ -627,22 +759,15 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
 
         // ---- batch reduction (NCCL across ranks: integer sums are exact)
         if (R.world > 1) {
-            NK(ncclGroupStart());
-            NK(ncclAllReduce(R.acc.k, R.acc.k, 3, ncclUint64, ncclSum, R.comm, R.main));
-            NK(ncclAllReduce(R.acc.counts, R.acc.counts, 8, ncclUint64, ncclSum, R.comm, R.main));
-            if (active)
-                NK(ncclAllReduce(R.acc.tally, R.acc.tally, 4 * (size_t)R.n_tally_bins, ncclUint64, ncclSum, R.comm,
-                                 R.main));
-            NK(ncclAllGather(R.acc.bank_count, R.d_sall, 1, ncclUint64, R.comm, R.main));
-            NK(ncclGroupEnd());
+            R.bc->reduce_batch(R, active);
         } else {
-            CK(cudaMemcpyAsync(R.d_sall, R.acc.bank_count, sizeof(ull), cudaMemcpyDeviceToDevice, R.main));
+            R.sall.assign(1, 0);
+            CK(cudaMemcpyAsync(R.sall.data(), R.acc.bank_count, sizeof(ull), cudaMemcpyDeviceToHost, R.main));
         }
+        const std::vector<ull>& sall = R.sall;
         ull hk[3], hc[8];
-        std::vector<ull> sall(R.world);
         CK(cudaMemcpyAsync(hk, R.acc.k, sizeof hk, cudaMemcpyDeviceToHost, R.main));
         CK(cudaMemcpyAsync(hc, R.acc.counts, sizeof hc, cudaMemcpyDeviceToHost, R.main));
-        CK(cudaMemcpyAsync(sall.data(), R.d_sall, sizeof(ull) * R.world, cudaMemcpyDeviceToHost, R.main));
         std::vector<ull> tb;
         if (active) {
             tb.resize(4 * (size_t)R.n_tally_bins);
@@ -680,21 +805,8 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
             // each rank needs a contiguous slice of the global canonical bank
             std::vector<int64_t> plan(4 * (size_t)R.world + 2);
             bank_exchange_plan(reinterpret_cast<const uint64_t*>(sall.data()), R.world, R.N, off, R.rank, plan.data());
-            const int W = R.world;
-            const uint64_t my_a = (uint64_t)plan[4 * W];
-            NK(ncclGroupStart());
-            for (int r = 0; r < W; ++r) {
-                int64_t sf = plan[r], sc = plan[W + r], rf = plan[2 * W + r], rc = plan[3 * W + r];
-                if (r == R.rank) {
-                    if (sc > 0)
-                        CK(cudaMemcpyAsync(R.recv + rf, R.canon + sf, sizeof(Site) * (size_t)sc,
-                                           cudaMemcpyDeviceToDevice, R.main));
-                    continue;
-                }
-                if (sc > 0) NK(ncclSend(R.canon + sf, sizeof(Site) * (size_t)sc, ncclChar, r, R.comm, R.main));
-                if (rc > 0) NK(ncclRecv(R.recv + rf, sizeof(Site) * (size_t)rc, ncclChar, r, R.comm, R.main));
-            }
-            NK(ncclGroupEnd());
+            const uint64_t my_a = (uint64_t)plan[4 * R.world];
+            R.bc->exchange(R, plan.data());
             launch_resample(R.recv, (int64_t)my_a, S_total, off, R.N, R.rank_lo, R.N_rank, R.source, R.main);
         }
         CK(cudaGetLastError());
@@ -708,12 +820,7 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, R.ev_a0, R.ev_a1));
     R.t_active = (double)ms * 1e-3;
-    if (R.world > 1) {  // max over ranks
-        CK(cudaMemcpyAsync(R.d_time, &R.t_active, sizeof(double), cudaMemcpyHostToDevice, R.main));
-        NK(ncclAllReduce(R.d_time, R.d_time, 1, ncclFloat64, ncclMax, R.comm, R.main));
-        CK(cudaMemcpyAsync(&R.t_active, R.d_time, sizeof(double), cudaMemcpyDeviceToHost, R.main));
-        CK(cudaStreamSynchronize(R.main));
-    }
+    if (R.world > 1) R.t_active = R.bc->max_over_ranks(R, R.t_active);  // max over ranks
 }
 
 void validate(const omcg_run_config& cfg) {
@@ -850,28 +957,40 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
     const int local_ranks = multiproc ? 1 : cfg.n_gpus;
     int ndev = device_count();
     std::vector<int> devs(local_ranks);
+    bool shared_gpu = false;  // local ranks on one GPU: in-process loopback instead of NCCL
     for (int i = 0; i < local_ranks; ++i) {
         devs[i] = cfg.devices[i];
         if (devs[i] < 0 || devs[i] >= ndev) throw CudaError("CUDA device " + std::to_string(devs[i]) + " not available");
         for (int j = 0; j < i; ++j)
-            if (devs[j] == devs[i]) throw std::invalid_argument("duplicate CUDA device in devices[]");
+            if (devs[j] == devs[i]) shared_gpu = true;
     }
+    std::vector<int> meter_devs = devs;
+    std::sort(meter_devs.begin(), meter_devs.end());
+    meter_devs.erase(std::unique(meter_devs.begin(), meter_devs.end()), meter_devs.end());
     EnergyMeter meter;
-    meter.start(devs);
+    meter.start(meter_devs);
     reset_launch_counter();
     std::vector<Rank> ranks(local_ranks);
     std::vector<ncclComm_t> comms(local_ranks, nullptr);
+    std::unique_ptr<LoopbackShared> loop_shared;
+    std::vector<std::unique_ptr<BatchComm>> bcs(local_ranks);
     if (multiproc) {
         ncclUniqueId id;
         std::memcpy(id.internal, cfg.nccl_id, 128);
         CK(cudaSetDevice(devs[0]));
         NK(ncclCommInitRank(&comms[0], cfg.world_size, id, cfg.rank));
+        bcs[0].reset(new NcclBatchComm());
+    } else if (local_ranks > 1 && shared_gpu) {
+        loop_shared.reset(new LoopbackShared(local_ranks));
+        for (int i = 0; i < local_ranks; ++i) bcs[i].reset(new LoopbackBatchComm(loop_shared.get()));
     } else if (local_ranks > 1) {
         NK(ncclCommInitAll(comms.data(), local_ranks, devs.data()));
+        for (int i = 0; i < local_ranks; ++i) bcs[i].reset(new NcclBatchComm());
     }
     for (int i = 0; i < local_ranks; ++i) {
         ranks[i].device = devs[i];
         ranks[i].comm = comms[i];
+        ranks[i].bc = bcs[i].get();
         ranks[i].world = multiproc ? cfg.world_size : local_ranks;
         ranks[i].rank = multiproc ? cfg.rank : i;
     }

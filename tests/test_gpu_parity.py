@@ -104,6 +104,10 @@ def test_queue_contents_bit_exact(kind, n, in_flight, tail, sort):
     dict(particles_in_flight=5000, tail_threshold=0),     # pure event-by-event
     dict(particles_in_flight=5000, tail_threshold=10**9),  # history-per-thread tail right after refill
     dict(mode="openmc-queueless", particles_in_flight=3000, tail_threshold=0),
+    # multi-rank path (partition, int64 reductions, fission-bank exchange plan)
+    # with ranks sharing GPU 0 through the in-process loopback transport
+    dict(particles_in_flight=5000, n_gpus=2, devices=[0, 0]),
+    dict(particles_in_flight=2000, n_gpus=3, devices=[0, 0, 0], tasks_per_gpu=2),
 ])
 def test_tuned_parameters_do_not_change_results(kw):
     """in-flight count (and every other tuned knob) changes time only."""
