@@ -27,6 +27,8 @@ struct Ctx {
     int tally_on;
     int n_tally_bins;
     int tally_smem;       // 1: aggregate tallies in shared memory (few bins)
+    unsigned long long* tally_priv;  // n_priv per-SM copies of the tally (folded per batch)
+    int n_priv;
     double k_norm;
     int64_t rank_lo;      // batch-global index of this rank's first history
     int64_t n_batch;      // histories per batch, whole job
@@ -68,6 +70,9 @@ void launch_collide(const Ctx& c, const int32_t* q, int n, int n_front, cudaStre
 // material/energy sort of the fuel XS queue (16-bit energy radix per material)
 void launch_sort(const Ctx& c, const int32_t* q_in, int32_t* q_out, int n, int n_fuel_mats,
                  unsigned int* hist, unsigned int* cursor, uint32_t* keys, unsigned int* bsum, cudaStream_t s);
+
+// tally[i] += sum of the n_priv private copies; copies zeroed
+void launch_tally_fold(unsigned long long* priv, int n_priv, int64_t n, unsigned long long* tally, cudaStream_t s);
 
 // fission bank: canonical order + systematic resampling
 void launch_scan_i32(const int32_t* in, int64_t* out, int64_t n, int64_t* tmp, cudaStream_t s);

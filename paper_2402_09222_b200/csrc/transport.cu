@@ -256,6 +256,8 @@ struct Rank {
     int64_t* scan_out = nullptr;
     int64_t* scan_tmp = nullptr;
     ull* d_sall = nullptr;  // allgathered bank counts
+    ull* tally_priv = nullptr;  // per-SM private tally copies
+    int n_priv = 0;
     double* d_time = nullptr;
     cudaStream_t main = nullptr;
     cudaEvent_t ev_a0 = nullptr, ev_a1 = nullptr;
@@ -273,6 +275,8 @@ struct Rank {
     std::string error;
 };
 
+bool env_flag(const char* name);  // unset or nonzero -> true
+
 // ------------------------------------------------------------------ setup
 void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     auto t0 = std::chrono::steady_clock::now();
@@ -289,6 +293,18 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     R.n_tally_bins = p.geo.nx * p.geo.ny;
     R.bank_cap = 3 * R.N_rank + 4096;
     R.acc.tally = R.arena.alloc<ull>(4 * (int64_t)R.n_tally_bins);
+    {   // per-SM private copies (bounded to 64 MB) unless tallies fit in shared memory
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, R.device);
+        const int64_t per = 4 * (int64_t)R.n_tally_bins * (int64_t)sizeof(ull);
+        R.n_priv = 4 * R.n_tally_bins <= SMEM_TALLY_MAX || !env_flag("OMCG_TALLY_PRIV")
+                       ? 0
+                       : (int)std::max<int64_t>(1, std::min<int64_t>(sms, (64LL << 20) / per));
+        if (R.n_priv > 0) {
+            R.tally_priv = R.arena.alloc<ull>((int64_t)R.n_priv * 4 * R.n_tally_bins);
+            CK(cudaMemset(R.tally_priv, 0, (size_t)R.n_priv * (size_t)per));
+        }
+    }
     R.acc.k = R.arena.alloc<ull>(3);
     R.acc.counts = R.arena.alloc<ull>(8);
     R.acc.bank = R.arena.alloc<Site>(R.bank_cap);
@@ -716,6 +732,8 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         base.tally_on = active ? 1 : 0;
         base.n_tally_bins = R.n_tally_bins;
         base.tally_smem = tally_smem;
+        base.tally_priv = R.tally_priv;
+        base.n_priv = R.n_priv;
         base.k_norm = k_norm;
         base.rank_lo = R.rank_lo;
         base.n_batch = R.N;
@@ -757,6 +775,8 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
             if (S.h_ctrl[2] & 2ULL) throw std::runtime_error("fission bank overflow");
         }
 
+        if (active && R.n_priv > 0)
+            launch_tally_fold(R.tally_priv, R.n_priv, 4 * (int64_t)R.n_tally_bins, R.acc.tally, R.main);
         // ---- batch reduction (NCCL across ranks: integer sums are exact)
         if (R.world > 1) {
             R.bc->reduce_batch(R, active);
