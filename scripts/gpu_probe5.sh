@@ -1,3 +1,2 @@
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
-OMCG_TALLY_PRIV=0 python scripts/run_c2.py 7 2
-OMCG_TALLY_PRIV=1 python scripts/run_c2.py 7 2
+python scripts/run_c2.py 7 2
