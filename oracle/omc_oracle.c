@@ -1119,11 +1119,13 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
     int64_t cap = in_flight < n_particles ? in_flight : n_particles;
     particle* slots = (particle*)malloc(sizeof(particle) * (size_t)cap);
     int* ev = (int*)malloc(sizeof(int) * (size_t)cap);
+    double* cache_E = (double*)malloc(sizeof(double) * (size_t)cap);
+    int* cache_m = (int*)calloc((size_t)cap, sizeof(int));
     accum A;
     memset(&A, 0, sizeof A);
     A.tally = (int64_t*)calloc(4 * (size_t)p->geo.nx * (size_t)p->geo.ny, sizeof(int64_t));
-    if (!slots || !ev || !A.tally) {
-        free(slots); free(ev); free(A.tally);
+    if (!slots || !ev || !A.tally || !cache_E || !cache_m) {
+        free(slots); free(ev); free(A.tally); free(cache_E); free(cache_m);
         return fail("out of memory");
     }
     for (int64_t s = 0; s < cap; ++s) ev[s] = Q_DEAD;
@@ -1147,12 +1149,20 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
                 chk += mix64((uint64_t)q->gidx + 1ULL);
                 int e = ev[s] <= Q_XS_NONFUEL ? EV_XS : ev[s] == Q_ADV ? EV_ADV : ev[s] == Q_CROSS ? EV_CROSS : EV_COLL;
                 do {  /* one event, or the whole remainder in the tail */
+                    const int prev = e;
                     switch (e) {
                     case EV_XS: e = ev_xs(p, q); break;
                     case EV_ADV: e = ev_advance(p, q, &A); break;
                     case EV_CROSS: e = ev_cross(p, q); break;
                     default: e = ev_collide(p, q, &A, 1.0); break;
                     }
+                    /* fuel cross-section cache: a history re-entering fuel at the energy of
+                     * its last fuel lookup takes that lookup's (identical) values at once
+                     * and goes straight to advance (OpenMC skips unchanged lookups too) */
+                    if (prev == EV_XS && p->mat[q->mat].fissionable) { cache_E[s] = q->E; cache_m[s] = q->mat; }
+                    if (prev == EV_CROSS && e == EV_XS && p->mat[q->mat].fissionable && cache_m[s] == q->mat &&
+                        cache_E[s] == q->E)
+                        e = ev_xs(p, q);
                 } while (tail && e != EV_DEAD);
                 ev[s] = e == EV_DEAD ? Q_DEAD : e == EV_XS ? (p->mat[q->mat].fissionable ? Q_XS_FUEL : Q_XS_NONFUEL)
                         : e == EV_ADV ? Q_ADV : e == EV_CROSS ? Q_CROSS : Q_COLL;
@@ -1170,6 +1180,7 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
             for (int64_t s = 0; s < cap && k > 0; ++s) {
                 if (ev[s] != Q_DEAD) continue;
                 if (init_particle(p, &slots[s], seed, 1, n_particles, next, NULL) != 0) { rc = -1; break; }
+                cache_E[s] = -1.0;
                 ev[s] = p->mat[slots[s].mat].fissionable ? Q_XS_FUEL : Q_XS_NONFUEL;
                 next++;
                 k--;
@@ -1178,7 +1189,7 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
         }
     }
     *n_out = n;
-    free(slots); free(ev); free(A.tally); free(A.bank);
+    free(slots); free(ev); free(A.tally); free(A.bank); free(cache_E); free(cache_m);
     return rc;
 }
 

@@ -58,9 +58,20 @@ struct alignas(128) PState {
 };
 static_assert(sizeof(PState) == 128, "PState must be one 128-byte line");
 
+// Last fuel macroscopic cross sections of a history. A history that leaves a
+// fuel pin and enters another without colliding has the same energy, so its
+// fuel calculate_xs is this cache (OpenMC skips the lookup on unchanged
+// material and energy too); the result is the same bits, the lookup is skipped.
+struct alignas(16) FuelCache {
+    double E, t, a, f, nf;
+    int32_t mat, pad;
+};
+static_assert(sizeof(FuelCache) == 48, "FuelCache layout");
+
 struct Bank {
     int64_t cap;
     PState* p;         // cap records
+    FuelCache* fc;     // cap fuel caches
     int4* cnt;         // per-slot event counters: n_xs, n_adv, n_cross, n_coll
     int8_t* event;     // dense next-event array (queueless sweeps, tail, refill)
     // running macroscopic total after every CKPT_STRIDE nuclides of a large
