@@ -1119,7 +1119,10 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
     int64_t cap = in_flight < n_particles ? in_flight : n_particles;
     particle* slots = (particle*)malloc(sizeof(particle) * (size_t)cap);
     int* ev = (int*)malloc(sizeof(int) * (size_t)cap);
-    double* cache_E = (double*)malloc(sizeof(double) * (size_t)cap);
+    /* per-slot cross-section cache: energy of the last lookup of each material,
+     * and the last many-nuclide (> SEG_LEN) material looked up (whose segment
+     * checkpoints the product keeps) */
+    double* cache_E = (double*)malloc(sizeof(double) * 3 * (size_t)cap);
     int* cache_m = (int*)calloc((size_t)cap, sizeof(int));
     accum A;
     memset(&A, 0, sizeof A);
@@ -1156,12 +1159,17 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
                     case EV_CROSS: e = ev_cross(p, q); break;
                     default: e = ev_collide(p, q, &A, 1.0); break;
                     }
-                    /* fuel cross-section cache: a history re-entering fuel at the energy of
-                     * its last fuel lookup takes that lookup's (identical) values at once
-                     * and goes straight to advance (OpenMC skips unchanged lookups too) */
-                    if (prev == EV_XS && p->mat[q->mat].fissionable) { cache_E[s] = q->E; cache_m[s] = q->mat; }
-                    if (prev == EV_CROSS && e == EV_XS && p->mat[q->mat].fissionable && cache_m[s] == q->mat &&
-                        cache_E[s] == q->E)
+                    /* cross-section cache: a history re-entering a material at the energy
+                     * of its last lookup of that material takes that lookup's (identical)
+                     * values at once and goes straight to advance (OpenMC skips unchanged
+                     * lookups too); a many-nuclide material only while it is still the
+                     * last many-nuclide material looked up */
+                    if (prev == EV_XS) {
+                        cache_E[3 * s + q->mat] = q->E;
+                        if (p->mat[q->mat].n > SEG_LEN) cache_m[s] = q->mat;
+                    }
+                    if (prev == EV_CROSS && e == EV_XS && cache_E[3 * s + q->mat] == q->E &&
+                        (p->mat[q->mat].n <= SEG_LEN || cache_m[s] == q->mat))
                         e = ev_xs(p, q);
                 } while (tail && e != EV_DEAD);
                 ev[s] = e == EV_DEAD ? Q_DEAD : e == EV_XS ? (p->mat[q->mat].fissionable ? Q_XS_FUEL : Q_XS_NONFUEL)
@@ -1180,7 +1188,8 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
             for (int64_t s = 0; s < cap && k > 0; ++s) {
                 if (ev[s] != Q_DEAD) continue;
                 if (init_particle(p, &slots[s], seed, 1, n_particles, next, NULL) != 0) { rc = -1; break; }
-                cache_E[s] = -1.0;
+                cache_E[3 * s] = cache_E[3 * s + 1] = cache_E[3 * s + 2] = -1.0;
+                cache_m[s] = -1;
                 ev[s] = p->mat[slots[s].mat].fissionable ? Q_XS_FUEL : Q_XS_NONFUEL;
                 next++;
                 k--;

@@ -58,20 +58,24 @@ struct alignas(128) PState {
 };
 static_assert(sizeof(PState) == 128, "PState must be one 128-byte line");
 
-// Last fuel macroscopic cross sections of a history. A history that leaves a
-// fuel pin and enters another without colliding has the same energy, so its
-// fuel calculate_xs is this cache (OpenMC skips the lookup on unchanged
-// material and energy too); the result is the same bits, the lookup is skipped.
-struct alignas(16) FuelCache {
-    double E, t, a, f, nf;
-    int32_t mat, pad;
+// Last macroscopic cross sections of a history per material (materials
+// 0..XS_CACHE_MATS-1). A history that crosses into a material it already
+// looked up at an unchanged energy (no collision since) takes the cached
+// values: same bits, lookup skipped (OpenMC skips unchanged lookups too).
+// ck_mat: the material whose segment checkpoints are in Bank::ckpt, so a
+// cached many-nuclide material is only reused when its checkpoints are current.
+constexpr int XS_CACHE_MATS = 3;
+struct alignas(128) XsCache {
+    double E[XS_CACHE_MATS];
+    int32_t ck_mat, pad;
+    double m[XS_CACHE_MATS][4];  // total, absorption, fission, nu-fission
 };
-static_assert(sizeof(FuelCache) == 48, "FuelCache layout");
+static_assert(sizeof(XsCache) == 128, "XsCache layout");
 
 struct Bank {
     int64_t cap;
     PState* p;         // cap records
-    FuelCache* fc;     // cap fuel caches
+    XsCache* xc;       // cap cross-section caches
     int4* cnt;         // per-slot event counters: n_xs, n_adv, n_cross, n_coll
     int8_t* event;     // dense next-event array (queueless sweeps, tail, refill)
     // running macroscopic total after every CKPT_STRIDE nuclides of a large

@@ -340,7 +340,7 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         Bank& B = S.b;
         B.p = A.alloc<PState>(cap);
         B.cnt = A.alloc<int4>(cap);
-        B.fc = A.alloc<FuelCache>(cap);
+        B.xc = A.alloc<XsCache>(cap);
         B.event = A.alloc<int8_t>(cap);
         B.ckpt = A.alloc<double>((int64_t)NCKPT * cap);
         CK(cudaMemsetAsync(B.event, EV_DEAD, (size_t)cap, S.stream));
