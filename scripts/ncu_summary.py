@@ -64,12 +64,22 @@ def main():
             "upper bounds and times are serialised single launches")
     json.dump({"note": note, "kernels": summary}, open(os.path.join(prof, f"{tag}_ncu_summary.json"), "w"),
               indent=1)
-    xs = summary.get("k_xs_fuel")
-    if xs:
-        items = xs["launch__grid_size"] * xs["launch__block_size"]
-        per = (xs["dram__bytes_read.sum"] + xs["dram__bytes_write.sum"]) / items
-        json.dump({"dram_bytes_per_item": per, "items_in_capture": items,
-                   "source": f"profiles/{tag}_ncu_summary.json (k_xs_fuel, cold cache, grid*block items)"},
+    # dram bytes per fuel lookup (queue entry) of the fuel calculate_xs launch(es) captured
+    xs_kernels = [k for k in ("k_xs_fuel", "k_xs_fuel_fused", "k_xs_fuel_seg", "k_xs_fuel_combine") if k in summary]
+    if xs_kernels:
+        nseg = int(os.environ.get("OMCG_FUEL_SEGMENTS", "17"))  # 261 fuel nuclides in 16-nuclide segments
+        # fuel lookups (queue entries) per block of each kernel
+        per_block = {"k_xs_fuel": None, "k_xs_fuel_combine": None, "k_xs_fuel_fused": 32,
+                     "k_xs_fuel_seg": 256 / nseg}
+        per, parts = 0.0, {}
+        for k in xs_kernels:
+            x = summary[k]
+            items = x["launch__grid_size"] * (per_block[k] or x["launch__block_size"])
+            b = (x["dram__bytes_read.sum"] + x["dram__bytes_write.sum"]) / items
+            parts[k] = {"lookups_in_capture": items, "dram_bytes_per_lookup": b}
+            per += b
+        json.dump({"dram_bytes_per_item": per, "kernels": parts,
+                   "source": f"profiles/{tag}_ncu_summary.json ({'+'.join(xs_kernels)}, cold cache)"},
                   open(os.path.join(prof, "xs_fuel_ncu.json"), "w"), indent=1)
     lc = os.path.join(src, "launches.csv")
     if os.path.exists(lc):
