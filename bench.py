@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--bins", type=int, default=4000)
     ap.add_argument("--sort", type=int, default=20_000)
     ap.add_argument("--tasks", type=int, default=1)
+    ap.add_argument("--event-fusion", type=int, default=1, choices=[0, 1],
+                    help="queued mode: 1 = move kernel for the non-fuel events, 0 = one kernel per event type")
     ap.add_argument("--cpu-sample", type=int, default=100_000, help="histories per CPU-baseline batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -56,6 +58,7 @@ def workload_config(a, world):
                     f"{a.problem}, {a.particles} histories/batch/GPU",
         "P0": a.mode, "P1": a.in_flight, "P2": a.bins, "P3": a.sort if a.mode == "openmc" else None,
         "P4": 8, "P5": a.tasks, "P6": "threads",
+        "event_fusion": a.event_fusion if a.mode == "openmc" else None,
         "histories_per_batch": a.particles * world,
         "parallelism": f"particle-bank dp{world}",
         "l2": "no flush needed: working set (122 MB library + ~170 MB in-flight bank) exceeds the 126 MB L2",
@@ -192,7 +195,8 @@ def main():
     out = P.run(problem, mode=a.mode, particles_in_flight=a.in_flight, n_bins=a.bins,
                 sort_threshold=a.sort if a.mode == "openmc" else None, host_threads=8, tasks_per_gpu=a.tasks,
                 n_particles=a.particles * world, n_batches=a.warmup + a.steps, n_inactive=a.warmup, seed=1,
-                world_size=world, rank=rank, nccl_id=nccl_id, devices=[local], profile=2)
+                world_size=world, rank=rank, nccl_id=nccl_id, devices=[local], profile=2,
+                event_fusion=a.event_fusion)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     # short separately-profiled pass (every kernel class timed) for the kernel shares only
@@ -200,7 +204,8 @@ def main():
     if world == 1:
         pr = P.run(problem, mode=a.mode, particles_in_flight=a.in_flight, n_bins=a.bins,
                    sort_threshold=a.sort if a.mode == "openmc" else None, host_threads=8, tasks_per_gpu=a.tasks,
-                   n_particles=a.particles, n_batches=3, n_inactive=1, seed=1, devices=[local], profile=1).result
+                   n_particles=a.particles, n_batches=3, n_inactive=1, seed=1, devices=[local], profile=1,
+                   event_fusion=a.event_fusion).result
         names = ["calculate_xs_fuel", "calculate_xs_nonfuel", "advance", "surface_crossing", "collision",
                  "sort", "refill", "tail"]
         tot = sum(pr.prof_ms[i] for i in range(8))

@@ -1104,7 +1104,11 @@ static void transport(const orc_problem* p, particle* q, accum* A, double k_norm
  * refills the slots that were empty at the start of the iteration from the
  * source; once the source is exhausted and at most
  * tail_threshold histories are alive, all of them are finished at once
- * (recorded as queue 5). Trace entries: (queue, length, sum of mix64(id+1)). */
+ * (recorded as queue 5). Trace entries: (queue, length, sum of mix64(id+1)).
+ * event_fusion (the product's default, omcg_run_config.event_fusion): the
+ * advance queue is the "move" queue — each of its histories runs events back
+ * to back until it needs a calculate_xs in a fissionable (fuel) material,
+ * collides in one, or dies; non-fuel lookups of new histories join it too. */
 enum { Q_XS_FUEL = 0, Q_XS_NONFUEL = 1, Q_ADV = 2, Q_CROSS = 3, Q_COLL = 4, Q_DEAD = 5 };
 
 static uint64_t mix64(uint64_t z) {
@@ -1114,7 +1118,7 @@ static uint64_t mix64(uint64_t z) {
 }
 
 int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, int64_t in_flight,
-                    int64_t tail_threshold, int64_t* out, int64_t max_entries, int64_t* n_out) {
+                    int64_t tail_threshold, int event_fusion, int64_t* out, int64_t max_entries, int64_t* n_out) {
     if (!p || !n_out || n_particles < 1 || in_flight < 1) return fail("invalid queue-trace arguments");
     int64_t cap = in_flight < n_particles ? in_flight : n_particles;
     particle* slots = (particle*)malloc(sizeof(particle) * (size_t)cap);
@@ -1145,6 +1149,7 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
             for (int k = 1; k < 5; ++k)
                 if (len[k] > len[best]) best = k;
             int tail = next >= n_particles && live <= tail_threshold;
+            int move = event_fusion && best == Q_ADV && !tail;
             uint64_t chk = 0;
             for (int64_t s = 0; s < cap; ++s) {
                 if (ev[s] == Q_DEAD || (!tail && ev[s] != best)) continue;
@@ -1171,7 +1176,8 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
                     if (prev == EV_CROSS && e == EV_XS && cache_E[3 * s + q->mat] == q->E &&
                         (p->mat[q->mat].n <= SEG_LEN || cache_m[s] == q->mat))
                         e = ev_xs(p, q);
-                } while (tail && e != EV_DEAD);
+                } while (e != EV_DEAD &&
+                         (tail || (move && !((e == EV_XS || e == EV_COLL) && p->mat[q->mat].fissionable))));
                 ev[s] = e == EV_DEAD ? Q_DEAD : e == EV_XS ? (p->mat[q->mat].fissionable ? Q_XS_FUEL : Q_XS_NONFUEL)
                         : e == EV_ADV ? Q_ADV : e == EV_CROSS ? Q_CROSS : Q_COLL;
             }
@@ -1190,7 +1196,7 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
                 if (init_particle(p, &slots[s], seed, 1, n_particles, next, NULL) != 0) { rc = -1; break; }
                 cache_E[3 * s] = cache_E[3 * s + 1] = cache_E[3 * s + 2] = -1.0;
                 cache_m[s] = -1;
-                ev[s] = p->mat[slots[s].mat].fissionable ? Q_XS_FUEL : Q_XS_NONFUEL;
+                ev[s] = p->mat[slots[s].mat].fissionable ? Q_XS_FUEL : event_fusion ? Q_ADV : Q_XS_NONFUEL;
                 next++;
                 k--;
             }

@@ -106,7 +106,7 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
                 host_threads=8, tasks_per_gpu=1, cpu_bind="threads", n_particles=1_000_000,
                 n_batches=15, n_inactive=5, seed=1, n_gpus=1, devices=None, world_size=1, rank=0,
                 nccl_id: bytes | None = None, record_batch=0, record_n=0, profile=False,
-                trace_queues=False, tail_threshold=None) -> RunConfig:
+                trace_queues=False, tail_threshold=None, event_fusion=None) -> RunConfig:
     cfg = RunConfig()
     _lib.omcg_run_config_default(C.byref(cfg))
     m = {"openmc": QUEUED, "queued": QUEUED, "openmc-queueless": QUEUELESS,
@@ -138,6 +138,8 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
     cfg.trace_queues = int(bool(trace_queues))
     if tail_threshold is not None:
         cfg.tail_threshold = int(tail_threshold)
+    if event_fusion is not None:
+        cfg.event_fusion = int(event_fusion)
     return cfg
 
 

@@ -130,6 +130,7 @@ OMCG_API void omcg_run_config_default(omcg_run_config* c) {
     c->world_size = 1;
     c->rank = 0;
     c->tail_threshold = 16384;
+    c->event_fusion = 1;
 }
 
 OMCG_API int omcg_run(const omcg_problem* p, const omcg_run_config* cfg, omcg_run_result* res, int64_t* tally_out,

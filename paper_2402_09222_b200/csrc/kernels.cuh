@@ -37,6 +37,7 @@ struct Ctx {
     int64_t record_n;
     int recording;
     unsigned long long* ctrl;  // [0] refill ticket, [1] alive, [2] error flags
+    int fused;                 // event fusion: non-fuel XS work goes to the move (advance) queue
 };
 
 constexpr int SMEM_TALLY_MAX = 64;  // tally bins*scores aggregated per block in smem (few-pin problems)
@@ -61,11 +62,19 @@ void launch_xs(const Ctx& c, const int32_t* q, int n, bool fuel, cudaStream_t s)
 // fuel-queue calculate_xs split by 16-nuclide segment (nseg segments, partial
 // sums in part[nseg][4][cap]) + an in-order fold; same arithmetic as launch_xs
 void launch_xs_fuel_split(const Ctx& c, const int32_t* q, int n, int nseg, double* part, cudaStream_t s);
+// the same split lookup in one launch: a block per 32 entries, segment
+// partials in shared memory, in-order fold by warp 0 (nseg <= 48)
+void launch_xs_fuel_fused(const Ctx& c, const int32_t* q, int n, int nseg, cudaStream_t s);
 void launch_advance(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 void launch_cross(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 // the collision queue is double-ended: n_front fuel entries at the front,
 // n - n_front non-fuel entries at the back
 void launch_collide(const Ctx& c, const int32_t* q, int n, int n_front, cudaStream_t s);
+
+// fused transport: every history of the move queue runs advance / crossing /
+// non-fuel calculate_xs / non-fuel collision in registers until it needs a
+// fuel lookup, collides in fuel or dies
+void launch_move(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 
 // material/energy sort of the fuel XS queue (16-bit energy radix per material)
 void launch_sort(const Ctx& c, const int32_t* q_in, int32_t* q_out, int n, int n_fuel_mats,

@@ -131,6 +131,7 @@ int main(int argc, char** argv) {
     cfg.n_batches = (int)env_ll("OMCG_BATCHES", cfg.n_batches);
     cfg.n_inactive = (int)env_ll("OMCG_INACTIVE", cfg.n_inactive);
     cfg.seed = (uint64_t)env_ll("OMCG_SEED", 1);
+    cfg.event_fusion = (int)env_ll("OMCG_EVENT_FUSION", cfg.event_fusion);
     const uint64_t xs_seed = (uint64_t)env_ll("OMCG_XS_SEED", 1234);
     const int want = (int)env_ll("OMCG_GPUS", 1);
     bind_cpus(cfg.cpu_bind, cfg.host_threads);

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <condition_variable>
 #include <memory>
@@ -276,16 +277,27 @@ struct Rank {
 };
 
 bool env_flag(const char* name);  // unset or nonzero -> true
+int xs_fuel_mode();
 
 // ------------------------------------------------------------------ setup
 void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     auto t0 = std::chrono::steady_clock::now();
+    static const bool trace_init = std::getenv("OMCG_TRACE_INIT") != nullptr;
+    auto mark = [&](const char* what) {
+        if (!trace_init) return;
+        cudaDeviceSynchronize();
+        std::fprintf(stderr, "[omcg init] %-28s %8.3f s\n", what,
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    };
     CK(cudaSetDevice(R.device));
+    mark("set device");
     R.arena.device = R.device;
     CK(cudaStreamCreateWithFlags(&R.main, cudaStreamNonBlocking));
     CK(cudaEventCreate(&R.ev_a0));
     CK(cudaEventCreate(&R.ev_a1));
+    mark("streams/events");
     R.gp.upload(p, cfg.n_bins, R.device, R.main);
+    mark("library upload + hash");
     R.h2d += R.gp.h2d_bytes;
     R.N = cfg.n_particles;
     R.rank_lo = R.N * R.rank / R.world;
@@ -321,6 +333,7 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     R.d_sall = R.arena.alloc<ull>(R.world);
     R.d_time = R.arena.alloc<double>(1);
     R.tally_total.assign(4 * (size_t)R.n_tally_bins, 0);
+    mark("rank buffers");
 
     const int tasks = std::max(1, cfg.tasks_per_gpu);
     R.subs.resize(tasks);
@@ -360,7 +373,7 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
             S.dead_head = 0;
         }
         S.q_sorted = A.alloc<int32_t>(cap);
-        S.part = A.alloc<double>((int64_t)R.gp.max_fuel_seg * 4 * cap);
+        if (xs_fuel_mode() == 1) S.part = A.alloc<double>((int64_t)R.gp.max_fuel_seg * 4 * cap);
         S.tail_list = A.alloc<int32_t>(cap);
         S.keys = A.alloc<uint32_t>(cap);
         S.hist = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
@@ -379,6 +392,7 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
             CK(cudaEventCreate(&e.b));
         }
         CK(cudaStreamSynchronize(S.stream));
+        mark("sub-bank");
     }
     CK(cudaStreamSynchronize(R.main));
     R.t_init = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -402,15 +416,17 @@ void teardown_rank(Rank& R) {
 }
 
 // ------------------------------------------------------------------ event loops
-// A/B switches: OMCG_XS_SPLIT=0 selects the one-history-per-thread fuel
-// lookup, OMCG_TAIL_WARP=0 the thread-per-history tail.
+// A/B switches: OMCG_XS_SPLIT / OMCG_XS_FUSED select the fuel lookup
+// variant, OMCG_TAIL_WARP=0 the thread-per-history tail.
 bool env_flag(const char* name) {
     const char* v = std::getenv(name);
     return !v || std::atoi(v) != 0;
 }
-bool xs_split() {
-    static const bool on = env_flag("OMCG_XS_SPLIT");
-    return on;
+// fuel calculate_xs variant: 2 fused split (default), 1 two-launch split
+// (OMCG_XS_FUSED=0), 0 one history per thread (OMCG_XS_SPLIT=0)
+int xs_fuel_mode() {
+    static const int m = !env_flag("OMCG_XS_SPLIT") ? 0 : !env_flag("OMCG_XS_FUSED") ? 1 : 2;
+    return m;
 }
 bool tail_warp() {
     static const bool on = env_flag("OMCG_TAIL_WARP");
@@ -508,13 +524,19 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                     }
                     {
                         Prof pf(S, prof, 0, n);
-                        if (xs_split()) launch_xs_fuel_split(c, qptr, n, R.gp.max_fuel_seg, S.part, S.stream);
+                        const int xm = xs_fuel_mode();
+                        if (xm == 2) launch_xs_fuel_fused(c, qptr, n, R.gp.max_fuel_seg, S.stream);
+                        else if (xm == 1) launch_xs_fuel_split(c, qptr, n, R.gp.max_fuel_seg, S.part, S.stream);
                         else launch_xs(c, qptr, n, true, S.stream);
                     }
                     if (prof) S.xs_fuel_bytes += (double)n * (44.0 + 100.0 * (double)fuel_nuc);
                     break;
                 case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, false, S.stream); } break;
-                case EV_ADV: { Prof pf(S, prof, 2, n); launch_advance(c, qptr, n, S.stream); } break;
+                case EV_ADV: {
+                    Prof pf(S, prof, 2, n);
+                    if (c.fused) launch_move(c, qptr, n, S.stream);
+                    else launch_advance(c, qptr, n, S.stream);
+                } break;
                 case EV_CROSS: { Prof pf(S, prof, 3, n); launch_cross(c, qptr, n, S.stream); } break;
                 default: {
                     Prof pf(S, prof, 4, n);
@@ -742,6 +764,7 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         base.master = cfg.seed;
         base.record_n = cfg.record_n;
         base.recording = (R.acc.records && batch == cfg.record_batch) ? 1 : 0;
+        base.fused = cfg.mode == OMCG_QUEUED && cfg.event_fusion ? 1 : 0;
         const Site* src = have_source ? R.source : nullptr;
         const bool prof = cfg.profile != 0 && active;
 
@@ -988,8 +1011,15 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
     std::vector<int> meter_devs = devs;
     std::sort(meter_devs.begin(), meter_devs.end());
     meter_devs.erase(std::unique(meter_devs.begin(), meter_devs.end()), meter_devs.end());
+    static const bool trace_init = std::getenv("OMCG_TRACE_INIT") != nullptr;
+    auto mark = [&](const char* what) {
+        if (trace_init)
+            std::fprintf(stderr, "[omcg run] %-28s %8.3f s\n", what,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_call0).count());
+    };
     EnergyMeter meter;
     meter.start(meter_devs);
+    mark("energy meter started");
     reset_launch_counter();
     std::vector<Rank> ranks(local_ranks);
     std::vector<ncclComm_t> comms(local_ranks, nullptr);
@@ -1030,6 +1060,7 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
         for (int i = 0; i < local_ranks; ++i) th.emplace_back(body, i);
         for (auto& t : th) t.join();
     }
+    mark("ranks done");
     std::exception_ptr first;
     for (auto& e : errs)
         if (e && !first) first = e;
@@ -1099,10 +1130,14 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
             for (auto& S : R0.subs) g_trace.insert(g_trace.end(), S.trace.begin(), S.trace.end());
         }
     }
+    mark("results gathered");
     for (auto& R : ranks) teardown_rank(R);
     for (auto c : comms)
         if (c) ncclCommDestroy(c);
+    ranks.clear();  // device memory back before the call returns
+    mark("teardown");
     res->energy_j = meter.stop_joules();
+    mark("energy meter stopped");
     res->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_call0).count();
     if (first) std::rethrow_exception(first);
 }

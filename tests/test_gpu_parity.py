@@ -70,24 +70,27 @@ def test_pincell_transport_bit_exact():
     _compare_runs(P.PINCELL, 20000, 4, 2, 2000, particles_in_flight=20000)
 
 
-def test_assembly_transport_bit_exact():
-    _compare_runs(P.ASSEMBLY, 4000, 3, 1, 1000, particles_in_flight=4000)
+@pytest.mark.parametrize("fusion", [1, 0])
+def test_assembly_transport_bit_exact(fusion):
+    _compare_runs(P.ASSEMBLY, 4000, 3, 1, 1000, particles_in_flight=4000, tail_threshold=100, event_fusion=fusion)
 
 
+@pytest.mark.parametrize("fusion", [1, 0])
 @pytest.mark.parametrize("kind,n,in_flight,tail,sort", [
     (P.PINCELL, 6000, 1500, 300, 0),       # refill active, sorted fuel queue, tail
     (P.PINCELL, 4000, 4000, 0, -1),        # all in flight, no tail
     (P.ASSEMBLY, 3000, 1000, 200, 500),
 ])
-def test_queue_contents_bit_exact(kind, n, in_flight, tail, sort):
+def test_queue_contents_bit_exact(kind, n, in_flight, tail, sort, fusion):
     """North star: queue contents match. Per queued-mode iteration, the chosen
     queue, its length and the order-free checksum of its history ids equal the
-    oracle's emulation of the same scheduling policy (batch 1)."""
+    oracle's emulation of the same scheduling policy (batch 1), with and
+    without event fusion (the move kernel)."""
     o = O.Problem(kind, 1234, 4000)
-    want = o.queue_trace(n, in_flight, tail, seed=1)
+    want = o.queue_trace(n, in_flight, tail, seed=1, event_fusion=bool(fusion))
     p = P.Problem(kind, 1234)
     out = P.run(p, n_particles=n, n_batches=1, n_inactive=0, seed=1, particles_in_flight=in_flight,
-                tail_threshold=tail, sort_threshold=sort, trace_queues=True)
+                tail_threshold=tail, sort_threshold=sort, trace_queues=True, event_fusion=fusion)
     got = out.queue_trace
     assert got.shape == want.shape
     assert np.array_equal(got, want)
@@ -101,7 +104,9 @@ def test_queue_contents_bit_exact(kind, n, in_flight, tail, sort):
     dict(particles_in_flight=5000, n_bins=100000),
     dict(mode="openmc-queueless", particles_in_flight=3000),  # P0
     dict(particles_in_flight=2000, tasks_per_gpu=2),      # P5
-    dict(particles_in_flight=5000, tail_threshold=0),     # pure event-by-event
+    dict(particles_in_flight=5000, tail_threshold=0),     # pure event-by-event (move kernel)
+    dict(particles_in_flight=5000, tail_threshold=0, event_fusion=0),  # one kernel per event type
+    dict(particles_in_flight=1000, event_fusion=0),
     dict(particles_in_flight=5000, tail_threshold=10**9),  # history-per-thread tail right after refill
     dict(mode="openmc-queueless", particles_in_flight=3000, tail_threshold=0),
     # multi-rank path (partition, int64 reductions, fission-bank exchange plan)
