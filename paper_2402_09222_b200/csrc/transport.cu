@@ -67,7 +67,54 @@ namespace {
 std::mutex g_trace_mu;
 std::vector<int64_t> g_trace;
 
-// Device allocations owned by one object, freed on destruction.
+// Device allocations owned by one object, freed on destruction. They come
+// from the device's stream-ordered memory pool with the release threshold
+// raised, so freeing returns the pages to the pool instead of unmapping them
+// (a synchronous cudaFree of ~1 GB of bank buffers cost 0.04-0.7 s per run);
+// a later run in the same process (the in-process evaluator, bench passes)
+// reuses them. Allocated on the legacy stream and synchronised at once, so
+// any stream may use the memory.
+void keep_pool_memory(int device) {
+    static std::mutex mu;
+    static bool done[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done[device] = true;
+}
+// Pinned host words (queue lengths, control flags) read back every
+// iteration. Kept for the life of the process and reused by later runs:
+// cudaFreeHost synchronises the device and measured 0-0.5 s per call.
+struct PinnedSlab {
+    std::mutex mu;
+    std::vector<void*> free_blocks;  // 64-byte blocks
+    void* get() {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!free_blocks.empty()) {
+            void* p = free_blocks.back();
+            free_blocks.pop_back();
+            return p;
+        }
+        void* p = nullptr;
+        CK(cudaMallocHost(&p, 64));
+        return p;
+    }
+    void put(void* p) {
+        if (!p) return;
+        std::lock_guard<std::mutex> lk(mu);
+        free_blocks.push_back(p);
+    }
+};
+PinnedSlab& pinned() {
+    static PinnedSlab* s = new PinnedSlab();  // never destroyed (process lifetime)
+    return *s;
+}
+
 struct DevArena {
     std::vector<void*> ptrs;
     int device = 0;
@@ -75,14 +122,16 @@ struct DevArena {
     T* alloc(int64_t n) {
         void* p = nullptr;
         if (n <= 0) n = 1;
-        CK(cudaMalloc(&p, sizeof(T) * (size_t)n));
+        keep_pool_memory(device);
+        CK(cudaMallocAsync(&p, sizeof(T) * (size_t)n, 0));
+        CK(cudaStreamSynchronize(0));  // usable from any stream from here on
         ptrs.push_back(p);
         return static_cast<T*>(p);
     }
     ~DevArena() {
         if (ptrs.empty()) return;
         cudaSetDevice(device);
-        for (void* p : ptrs) cudaFree(p);
+        for (void* p : ptrs) cudaFreeAsync(p, 0);
     }
 };
 
@@ -380,12 +429,12 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         S.cursor = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
         S.bsum = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 64);
         CK(cudaMemsetAsync(S.hist, 0, sizeof(unsigned) * (size_t)R.gp.n_fuel_mats * 65536, S.stream));
-        S.ctrl = A.alloc<ull>(4);
+        S.ctrl = A.alloc<ull>(8);
         S.trace_chk = A.alloc<ull>(1);
-        CK(cudaMemsetAsync(S.ctrl, 0, sizeof(ull) * 4, S.stream));
-        CK(cudaMallocHost(&S.h_counts, sizeof(unsigned) * 8));
-        CK(cudaMallocHost(&S.h_ctrl, sizeof(ull) * 4));
-        CK(cudaMallocHost(&S.h_trace_chk, sizeof(ull)));
+        CK(cudaMemsetAsync(S.ctrl, 0, sizeof(ull) * 8, S.stream));
+        S.h_counts = static_cast<unsigned*>(pinned().get());  // 8 words
+        S.h_ctrl = static_cast<ull*>(pinned().get());         // 4 words
+        S.h_trace_chk = static_cast<ull*>(pinned().get());
         S.evs.resize(64);
         for (auto& e : S.evs) {
             CK(cudaEventCreate(&e.a));
@@ -400,19 +449,30 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
 
 void teardown_rank(Rank& R) {
     cudaSetDevice(R.device);
+    static const bool trace_init = std::getenv("OMCG_TRACE_INIT") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (trace_init)
+            std::fprintf(stderr, "[omcg teardown] %-22s %8.3f s\n", what,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    };
     for (auto& S : R.subs) {
         if (S.stream) cudaStreamDestroy(S.stream);
-        if (S.h_counts) cudaFreeHost(S.h_counts);
-        if (S.h_ctrl) cudaFreeHost(S.h_ctrl);
-        if (S.h_trace_chk) cudaFreeHost(S.h_trace_chk);
+        mark("stream");
+        pinned().put(S.h_counts);
+        pinned().put(S.h_ctrl);
+        pinned().put(S.h_trace_chk);
+        mark("host buffers");
         for (auto& e : S.evs) {
             if (e.a) cudaEventDestroy(e.a);
             if (e.b) cudaEventDestroy(e.b);
         }
     }
+    mark("events");
     if (R.main) cudaStreamDestroy(R.main);
     if (R.ev_a0) cudaEventDestroy(R.ev_a0);
     if (R.ev_a1) cudaEventDestroy(R.ev_a1);
+    mark("main stream");
 }
 
 // ------------------------------------------------------------------ event loops
@@ -1132,6 +1192,7 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
     }
     mark("results gathered");
     for (auto& R : ranks) teardown_rank(R);
+    mark("streams/events destroyed");
     for (auto c : comms)
         if (c) ncclCommDestroy(c);
     ranks.clear();  // device memory back before the call returns
