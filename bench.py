@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--tasks", type=int, default=1)
     ap.add_argument("--event-fusion", type=int, default=1, choices=[0, 1],
                     help="queued mode: 1 = move kernel for the non-fuel events, 0 = one kernel per event type")
+    ap.add_argument("--tail", type=int, default=None, help="tail threshold (histories; default: library default)")
     ap.add_argument("--cpu-sample", type=int, default=100_000, help="histories per CPU-baseline batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -196,7 +197,7 @@ def main():
                 sort_threshold=a.sort if a.mode == "openmc" else None, host_threads=8, tasks_per_gpu=a.tasks,
                 n_particles=a.particles * world, n_batches=a.warmup + a.steps, n_inactive=a.warmup, seed=1,
                 world_size=world, rank=rank, nccl_id=nccl_id, devices=[local], profile=2,
-                event_fusion=a.event_fusion)
+                event_fusion=a.event_fusion, tail_threshold=a.tail)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     # short separately-profiled pass (every kernel class timed) for the kernel shares only
@@ -205,7 +206,7 @@ def main():
         pr = P.run(problem, mode=a.mode, particles_in_flight=a.in_flight, n_bins=a.bins,
                    sort_threshold=a.sort if a.mode == "openmc" else None, host_threads=8, tasks_per_gpu=a.tasks,
                    n_particles=a.particles, n_batches=3, n_inactive=1, seed=1, devices=[local], profile=1,
-                   event_fusion=a.event_fusion).result
+                   event_fusion=a.event_fusion, tail_threshold=a.tail).result
         names = ["calculate_xs_fuel", "calculate_xs_nonfuel", "advance", "surface_crossing", "collision",
                  "sort", "refill", "tail"]
         tot = sum(pr.prof_ms[i] for i in range(8))
