@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--sort", type=int, default=20_000)
     ap.add_argument("--tasks", type=int, default=1)
     ap.add_argument("--event-fusion", type=int, default=1, choices=[0, 1],
-                    help="queued mode: 1 = move kernel for the non-fuel events, 0 = one kernel per event type")
+                    help="1 = move kernel for the non-fuel events, 0 = one kernel per event type")
     ap.add_argument("--tail", type=int, default=None, help="tail threshold (histories; default: library default)")
     ap.add_argument("--cpu-sample", type=int, default=100_000, help="histories per CPU-baseline batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -59,7 +59,7 @@ def workload_config(a, world):
                     f"{a.problem}, {a.particles} histories/batch/GPU",
         "P0": a.mode, "P1": a.in_flight, "P2": a.bins, "P3": a.sort if a.mode == "openmc" else None,
         "P4": 8, "P5": a.tasks, "P6": "threads",
-        "event_fusion": a.event_fusion if a.mode == "openmc" else None,
+        "event_fusion": a.event_fusion,
         "histories_per_batch": a.particles * world,
         "parallelism": f"particle-bank dp{world}",
         "l2": "no flush needed: working set (122 MB library + ~170 MB in-flight bank) exceeds the 126 MB L2",

@@ -96,12 +96,14 @@ typedef struct {
      * alive, finish them in one history-per-thread launch instead of one
      * launch per event (results are identical; 0 disables). */
     int64_t tail_threshold;
-    /* Queued mode only. 0: one kernel per event type (advance, crossing,
-     * non-fuel and fuel calculate_xs, collision), each history re-queued after
-     * every event. 1 (default): event fusion — the cheap events (advance,
-     * crossing, non-fuel calculate_xs and collision) of a history run back to
-     * back in one "move" kernel; only fuel calculate_xs and fuel collisions
-     * are queued separately. Results are identical either way. */
+    /* 0: one kernel per event type (advance, crossing, non-fuel and fuel
+     * calculate_xs, collision): queued mode re-queues each history after every
+     * event, queueless mode sweeps each of those kernels over all slots.
+     * 1 (default): event fusion — the cheap events (advance, crossing,
+     * non-fuel calculate_xs and collision) of a history run back to back in
+     * one "move" kernel; only fuel calculate_xs and fuel collisions are
+     * separate kernels (queued: separate queues; queueless: separate sweeps).
+     * Results are identical either way. */
     int event_fusion;
 } omcg_run_config;
 

@@ -632,10 +632,17 @@ void run_queueless(Rank& R, SubBank& S, Ctx c, const Site* src, bool prof, int64
             Prof pf(S, prof, 6, S.b.cap);
             launch_refill_all(c, next, remaining, src, S.stream);
         }
-        { Prof pf(S, prof, 0, S.b.cap); launch_xs(c, nullptr, 0, false, S.stream); }
-        { Prof pf(S, prof, 2, S.b.cap); launch_advance(c, nullptr, 0, S.stream); }
-        { Prof pf(S, prof, 3, S.b.cap); launch_cross(c, nullptr, 0, S.stream); }
-        { Prof pf(S, prof, 4, S.b.cap); launch_collide(c, nullptr, 0, 0, S.stream); }
+        if (c.fused) {  // sweeps of the fused kernels: fuel lookups, move, fuel collisions
+            const int cap = (int)S.b.cap;
+            { Prof pf(S, prof, 0, cap); launch_xs_fuel_fused(c, nullptr, cap, R.gp.max_fuel_seg, S.stream); }
+            { Prof pf(S, prof, 2, cap); launch_move(c, nullptr, cap, S.stream); }
+            { Prof pf(S, prof, 4, cap); launch_collide(c, nullptr, 0, 0, S.stream); }
+        } else {
+            { Prof pf(S, prof, 0, S.b.cap); launch_xs(c, nullptr, 0, false, S.stream); }
+            { Prof pf(S, prof, 2, S.b.cap); launch_advance(c, nullptr, 0, S.stream); }
+            { Prof pf(S, prof, 3, S.b.cap); launch_cross(c, nullptr, 0, S.stream); }
+            { Prof pf(S, prof, 4, S.b.cap); launch_collide(c, nullptr, 0, 0, S.stream); }
+        }
         CK(cudaMemcpyAsync(S.h_ctrl, S.ctrl, sizeof(ull) * 3, cudaMemcpyDeviceToHost, S.stream));
         CK(cudaStreamSynchronize(S.stream));
         if (prof) drain_profile(S);
@@ -824,7 +831,7 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         base.master = cfg.seed;
         base.record_n = cfg.record_n;
         base.recording = (R.acc.records && batch == cfg.record_batch) ? 1 : 0;
-        base.fused = cfg.mode == OMCG_QUEUED && cfg.event_fusion ? 1 : 0;
+        base.fused = cfg.event_fusion ? 1 : 0;
         const Site* src = have_source ? R.source : nullptr;
         const bool prof = cfg.profile != 0 && active;
 

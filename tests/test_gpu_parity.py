@@ -109,6 +109,8 @@ def test_queue_contents_bit_exact(kind, n, in_flight, tail, sort, fusion):
     dict(particles_in_flight=1000, event_fusion=0),
     dict(particles_in_flight=5000, tail_threshold=10**9),  # history-per-thread tail right after refill
     dict(mode="openmc-queueless", particles_in_flight=3000, tail_threshold=0),
+    dict(mode="openmc-queueless", particles_in_flight=3000, tail_threshold=0, event_fusion=0),
+    dict(mode="openmc-queueless", particles_in_flight=1000, tail_threshold=200, event_fusion=0),
     # multi-rank path (partition, int64 reductions, fission-bank exchange plan)
     # with ranks sharing GPU 0 through the in-process loopback transport
     dict(particles_in_flight=5000, n_gpus=2, devices=[0, 0]),
