@@ -21,8 +21,10 @@
  *           banking nu*sigma_f/sigma_t/k per collision.
  *
  * Determinism rules (shared with the CUDA product by specification, not by
- * code): compile with -ffp-contract=off; only + - * / sqrt and the two
- * polynomial transcendental functions below; int64 fixed-point tallies.
+ * code): compile with -ffp-contract=off; only + - * / sqrt, explicit fma()
+ * where written (log/exp polynomials, XS interpolation and accumulation) and
+ * the two polynomial transcendental functions below — all correctly rounded
+ * IEEE operations; int64 fixed-point tallies.
  */
 #define _GNU_SOURCE
 #include "omc_oracle.h"
@@ -100,43 +102,43 @@ double orc_log(double x) {
     double s = (m - 1.0) / (m + 1.0);
     double s2 = s * s;
     double p = 1.0 / 23.0;
-    p = p * s2 + 1.0 / 21.0;
-    p = p * s2 + 1.0 / 19.0;
-    p = p * s2 + 1.0 / 17.0;
-    p = p * s2 + 1.0 / 15.0;
-    p = p * s2 + 1.0 / 13.0;
-    p = p * s2 + 1.0 / 11.0;
-    p = p * s2 + 1.0 / 9.0;
-    p = p * s2 + 1.0 / 7.0;
-    p = p * s2 + 1.0 / 5.0;
-    p = p * s2 + 1.0 / 3.0;
-    double r = 2.0 * s + 2.0 * s * (s2 * p);
+    p = fma(p, s2, 1.0 / 21.0);
+    p = fma(p, s2, 1.0 / 19.0);
+    p = fma(p, s2, 1.0 / 17.0);
+    p = fma(p, s2, 1.0 / 15.0);
+    p = fma(p, s2, 1.0 / 13.0);
+    p = fma(p, s2, 1.0 / 11.0);
+    p = fma(p, s2, 1.0 / 9.0);
+    p = fma(p, s2, 1.0 / 7.0);
+    p = fma(p, s2, 1.0 / 5.0);
+    p = fma(p, s2, 1.0 / 3.0);
+    double r = fma(2.0 * s, s2 * p, 2.0 * s);
     double de = (double)e;
-    return de * LN2_HI + (r + de * LN2_LO);
+    return fma(de, LN2_HI, fma(de, LN2_LO, r));
 }
 
 /* exp(x): x = k ln2 + r, |r| <= ln2/2, Taylor to r^14, scale by 2^k. */
 double orc_exp(double x) {
     if (x > 709.0) return INFINITY;
     if (x < -708.0) return 0.0;
-    double kd = floor(x * INV_LN2 + 0.5);
+    double kd = floor(fma(x, INV_LN2, 0.5));
     int k = (int)kd;
-    double r = (x - kd * LN2_HI) - kd * LN2_LO;
+    double r = fma(-kd, LN2_LO, fma(-kd, LN2_HI, x));
     double p = 1.0 / 87178291200.0; /* 1/14! */
-    p = p * r + 1.0 / 6227020800.0;
-    p = p * r + 1.0 / 479001600.0;
-    p = p * r + 1.0 / 39916800.0;
-    p = p * r + 1.0 / 3628800.0;
-    p = p * r + 1.0 / 362880.0;
-    p = p * r + 1.0 / 40320.0;
-    p = p * r + 1.0 / 5040.0;
-    p = p * r + 1.0 / 720.0;
-    p = p * r + 1.0 / 120.0;
-    p = p * r + 1.0 / 24.0;
-    p = p * r + 1.0 / 6.0;
-    p = p * r + 0.5;
-    p = p * r + 1.0;
-    p = p * r + 1.0;
+    p = fma(p, r, 1.0 / 6227020800.0);
+    p = fma(p, r, 1.0 / 479001600.0);
+    p = fma(p, r, 1.0 / 39916800.0);
+    p = fma(p, r, 1.0 / 3628800.0);
+    p = fma(p, r, 1.0 / 362880.0);
+    p = fma(p, r, 1.0 / 40320.0);
+    p = fma(p, r, 1.0 / 5040.0);
+    p = fma(p, r, 1.0 / 720.0);
+    p = fma(p, r, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
     /* multiply by 2^k in two steps so k in [-1022-52, 1023] stays exact */
     int k1 = k / 2, k2 = k - k / 2;
     double s1 = bitsd((uint64_t)(k1 + 1023) << 52);
@@ -676,7 +678,7 @@ static inline int grid_index(const orc_problem* p, int n, double E, int b, doubl
 
 static inline double interp(const double* xs, int i, int c, double f) {
     double a = xs[4 * (size_t)i + c], b = xs[4 * (size_t)(i + 1) + c];
-    return a + f * (b - a);
+    return fma(f, b - a, a);
 }
 
 /* Macroscopic sums are segmented: the material's nuclides (in material order)
@@ -698,7 +700,7 @@ static void macro_xs(const orc_problem* p, int m, double E, double out[4]) {
             int i = grid_index(p, n, E, b, &f);
             const double* xs = p->nuc[n].xs;
             double d = M->dens[q];
-            for (int c = 0; c < 4; ++c) seg[c] = seg[c] + d * interp(xs, i, c, f);
+            for (int c = 0; c < 4; ++c) seg[c] = fma(d, interp(xs, i, c, f), seg[c]);
         }
         for (int c = 0; c < 4; ++c) acc[c] = acc[c] + seg[c];
     }
@@ -1014,7 +1016,7 @@ static int ev_collide(const orc_problem* p, particle* q, accum* A, double k_norm
             double f;
             int n = M->nuc[j];
             int i = grid_index(p, n, q->E, b, &f);
-            seg = seg + M->dens[j] * interp(p->nuc[n].xs, i, 0, f);
+            seg = fma(M->dens[j], interp(p->nuc[n].xs, i, 0, f), seg);
             if (acc + seg > cutoff) { sel = j; found = 1; break; }
         }
         acc = acc + seg;
