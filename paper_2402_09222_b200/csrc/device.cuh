@@ -80,7 +80,9 @@ struct Bank {
     int8_t* event;     // dense next-event array (queueless sweeps, tail, refill)
     // running macroscopic total after every CKPT_STRIDE nuclides of a large
     // material (written by calculate_xs, read by collision to jump straight
-    // to the segment holding the sampled nuclide): NCKPT x cap
+    // to the segment holding the sampled nuclide): cap x NCKPT, one 128-byte
+    // line per slot (queue order is random in slots, so a slot-major layout
+    // touches one line per lookup instead of NCKPT scattered sectors)
     double* ckpt;
 };
 constexpr int CKPT_STRIDE = 16;
