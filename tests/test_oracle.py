@@ -150,3 +150,27 @@ def test_pincell_physics_sanity():
     assert flux > 0 and absr > 0 and fis > 0 and nufis > 2 * fis
     # absorption rate per source particle ~ 1 (every history ends absorbed) within tally noise
     assert abs(absr / (4 * 20000) - 1.0) < 0.05
+
+
+@pytest.mark.parametrize("kind", [O.PINCELL, O.ASSEMBLY])
+def test_queue_trace_consistent_with_history_transport(kind):
+    """Two independent oracle code paths agree: with one kernel per event and no
+    tail, the queued emulation (orc_queue_trace) visits the advance, crossing
+    and collision queues exactly as often as the history-based transport
+    (orc_run) counts those events; with event fusion only the fuel lookup,
+    move and collision queues (and the tail) ever run, and fewer iterations."""
+    n = 3000
+    p = O.Problem(kind, 1234, 4000)
+    res, _, _ = p.run(n, 1, 0, seed=1, threads=0)
+    t0 = p.queue_trace(n, n, 0, seed=1, event_fusion=False)
+    tot = {q: int(t0[t0[:, 0] == q, 1].sum()) for q in range(6)}
+    assert tot[2] == res.n_events[1]  # advance
+    assert tot[3] == res.n_events[2]  # crossing
+    assert tot[4] == res.n_events[3]  # collision
+    assert tot[0] + tot[1] <= res.n_events[0]  # lookups (cache hits skip the queue)
+    t1 = p.queue_trace(n, n, 0, seed=1, event_fusion=True)
+    assert set(np.unique(t1[:, 0])) <= {0, 2, 4}
+    assert len(t1) < len(t0)
+    assert int(t1[t1[:, 0] == 4, 1].sum()) <= res.n_events[3]
+    # every history enters the move queue at least once; id checksums are order-free sums
+    assert int(t1[t1[:, 0] == 2, 1].sum()) >= n
