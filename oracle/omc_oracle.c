@@ -687,59 +687,25 @@ static inline double interp(const double* xs, int i, int c, double f) {
  * units of work for the GPU; for materials of <= SEG_LEN nuclides this is the
  * plain sequential sum.) */
 #define SEG_LEN 16
-#define MAX_CKPT 16 /* segment checkpoints kept per history (the product's NCKPT) */
-/* One segment's sums. Materials of <= SEG_LEN nuclides: sequential
- * (seg = fma(rho, xs, seg) in nuclide order). Materials of more (the depleted
- * fuel): a pairwise tree over the SEG_LEN slots of the segment, zero-padded,
- * evaluated as a binary counter — after slot j the partial of the lowest clear
- * bit level is formed by adding (left + right) — so that the GPU can evaluate
- * it lane-parallel (lane = nuclide, xor-butterfly: a + b == b + a and x + 0 == x
- * exactly for these non-negative terms). */
-static void segment_sums(const orc_problem* p, const material* M, int s0, int s1, double E, int b,
-                         double seg[4]) {
-    if (M->n <= SEG_LEN) {
-        for (int c = 0; c < 4; ++c) seg[c] = 0.0;
+static void macro_xs(const orc_problem* p, int m, double E, double out[4]) {
+    const material* M = &p->mat[m];
+    int b = bin_of(p, E);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int s0 = 0; s0 < M->n; s0 += SEG_LEN) {
+        double seg[4] = {0.0, 0.0, 0.0, 0.0};
+        int s1 = s0 + SEG_LEN < M->n ? s0 + SEG_LEN : M->n;
         for (int q = s0; q < s1; ++q) {
             int n = M->nuc[q];
             double f;
             int i = grid_index(p, n, E, b, &f);
-            for (int c = 0; c < 4; ++c) seg[c] = fma(M->dens[q], interp(p->nuc[n].xs, i, c, f), seg[c]);
+            const double* xs = p->nuc[n].xs;
+            double d = M->dens[q];
+            for (int c = 0; c < 4; ++c) seg[c] = fma(d, interp(xs, i, c, f), seg[c]);
         }
-        return;
-    }
-    double lv[5][4]; /* pending partial sums by tree level */
-    for (int j = 0; j < SEG_LEN; ++j) {
-        double v[4] = {0.0, 0.0, 0.0, 0.0};
-        if (s0 + j < s1) {
-            int q = s0 + j, n = M->nuc[q];
-            double f;
-            int i = grid_index(p, n, E, b, &f);
-            for (int c = 0; c < 4; ++c) v[c] = M->dens[q] * interp(p->nuc[n].xs, i, c, f);
-        }
-        int lvl = 0;
-        for (int k = j; k & 1; k >>= 1, ++lvl)
-            for (int c = 0; c < 4; ++c) v[c] = lv[lvl][c] + v[c];
-        for (int c = 0; c < 4; ++c) lv[lvl][c] = v[c];
-    }
-    for (int c = 0; c < 4; ++c) seg[c] = lv[4][c]; /* SEG_LEN = 16 = 2^4 */
-}
-
-static void macro_xs_ck(const orc_problem* p, int m, double E, double out[4], double* ck, int* nck) {
-    const material* M = &p->mat[m];
-    int b = bin_of(p, E);
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int k = 0;
-    for (int s0 = 0; s0 < M->n; s0 += SEG_LEN, ++k) {
-        double seg[4];
-        int s1 = s0 + SEG_LEN < M->n ? s0 + SEG_LEN : M->n;
-        segment_sums(p, M, s0, s1, E, b, seg);
         for (int c = 0; c < 4; ++c) acc[c] = acc[c] + seg[c];
-        if (ck && s1 < M->n) ck[k] = acc[0]; /* folded total after segment k */
     }
-    if (nck) *nck = k - 1;
     for (int c = 0; c < 4; ++c) out[c] = acc[c];
 }
-static void macro_xs(const orc_problem* p, int m, double E, double out[4]) { macro_xs_ck(p, m, E, out, NULL, NULL); }
 
 int orc_hash_bin(const orc_problem* p, double E) { return bin_of(p, E); }
 int orc_micro_xs(const orc_problem* p, int nuc, double E, int32_t* idx, double xs[4]) {
@@ -762,8 +728,6 @@ int orc_macro_xs(const orc_problem* p, int mat, double E, double xs[4]) {
 typedef struct {
     double x, y, z, u, v, w, E, wgt;
     double st, sa, sf, snf;
-    double ck[MAX_CKPT]; /* folded segment totals of the last calculate_xs (many-nuclide materials) */
-    int nck;
     uint64_t seed;
     int gx, gy, ring, mat, surf;
     int n_xs, n_adv, n_cross, n_coll, n_sites, term;
@@ -952,11 +916,8 @@ static void distance_to_boundary(const orc_problem* p, const particle* q, double
 }
 
 static int ev_xs(const orc_problem* p, particle* q) {
-    double m[4], ck[64];
-    int nck = 0;
-    macro_xs_ck(p, q->mat, q->E, m, ck, &nck);
-    q->nck = nck < MAX_CKPT ? nck : MAX_CKPT;
-    for (int k = 0; k < q->nck; ++k) q->ck[k] = ck[k];
+    double m[4];
+    macro_xs(p, q->mat, q->E, m);
     q->st = m[0]; q->sa = m[1]; q->sf = m[2]; q->snf = m[3];
     q->n_xs++;
     return EV_ADV;
@@ -1046,27 +1007,19 @@ static int ev_collide(const orc_problem* p, particle* q, accum* A, double k_norm
      * with the same segmented sums as macro_xs: cum = (folded earlier segments)
      * + (running sum inside the current segment) */
     double cutoff = orc_prn(&q->seed) * q->st;
-    /* the segment holding the sampled nuclide: the first whose folded total
-     * (the macro_xs checkpoints, up to MAX_CKPT of them) exceeds the cutoff;
-     * inside it the running sum is sequential; if it never exceeds the cutoff
-     * (rounding) the segment's last nuclide is taken */
     double acc = 0.0;
-    int jstart = 0;
-    if (M->n > SEG_LEN) /* checkpoints of this material at this energy: the preceding calculate_xs */
-        for (int k = 0; k < q->nck; ++k) {
-            if (q->ck[k] > cutoff) break;
-            acc = q->ck[k];
-            jstart = (k + 1) * SEG_LEN;
+    int sel = M->n - 1, found = 0;
+    for (int s0 = 0; s0 < M->n && !found; s0 += SEG_LEN) {
+        int s1 = s0 + SEG_LEN < M->n ? s0 + SEG_LEN : M->n;
+        double seg = 0.0;
+        for (int j = s0; j < s1; ++j) {
+            double f;
+            int n = M->nuc[j];
+            int i = grid_index(p, n, q->E, b, &f);
+            seg = fma(M->dens[j], interp(p->nuc[n].xs, i, 0, f), seg);
+            if (acc + seg > cutoff) { sel = j; found = 1; break; }
         }
-    int jend = jstart + SEG_LEN < M->n ? jstart + SEG_LEN : M->n;
-    int sel = jend - 1;
-    double seg = 0.0;
-    for (int j = jstart; j < jend; ++j) {
-        double f;
-        int n = M->nuc[j];
-        int i = grid_index(p, n, q->E, b, &f);
-        seg = fma(M->dens[j], interp(p->nuc[n].xs, i, 0, f), seg);
-        if (acc + seg > cutoff) { sel = j; break; }
+        acc = acc + seg;
     }
     int n = M->nuc[sel];
     double f;
