@@ -1128,6 +1128,7 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
         for (auto& t : th) t.join();
     }
     mark("ranks done");
+    if (std::getenv("OMCG_MOVE_CYCLES")) dump_move_cycles();
     std::exception_ptr first;
     for (auto& e : errs)
         if (e && !first) first = e;
