@@ -12,7 +12,7 @@ r = P.run(p, n_particles=1000000, n_batches=2, n_inactive=1).result
 print("FoM", r.fom)
 PY
 timeout 900 ncu --metrics gpu__time_duration.sum,launch__grid_size,launch__block_size --clock-control none --csv --log-file gpurun_out/launches.csv python /tmp/run2.py > /dev/null 2>&1
-for k in k_move:8 k_xs_fuel_fused:10 k_collide:8 k_tail_warp:0 k_sort_scatter:6; do
+for k in k_move:8 k_xs_fuel_fused:10 k_collide:8 k_tail_warp:0 k_sort_scatter:6 k_sort_hist:6; do
   name=${k%%:*}; skip=${k##*:}
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^${name}\$" -s $skip -c 1 -o gpurun_out/r01_${name} python /tmp/run2.py > gpurun_out/ncu_${name}.log 2>&1; tail -1 gpurun_out/ncu_${name}.log
 done
