@@ -534,11 +534,25 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
     const bool trace = cfg.trace_queues != 0;
     const int64_t tail = cfg.tail_threshold;
     bool pending_trace = false;
+    // A fuel calculate_xs launch moves every one of its n entries to the move
+    // queue (count[EV_ADV] += n, count[EV_XS_FUEL] = 0) and changes nothing
+    // else, so after such an iteration (without a refill) the host knows the
+    // next queue lengths exactly and skips the read-back and its sync.
+    bool known = false, check_prediction = false;
+    unsigned predicted[8];
+    static const bool predict = env_flag("OMCG_PREDICT_COUNTS");
     for (;;) {
-        CK(cudaMemcpyAsync(S.h_counts, S.qs.count, sizeof(unsigned) * 8, cudaMemcpyDeviceToHost, S.stream));
-        if (pending_trace) CK(cudaMemcpyAsync(S.h_trace_chk, S.trace_chk, sizeof(ull), cudaMemcpyDeviceToHost, S.stream));
-        CK(cudaStreamSynchronize(S.stream));
-        if (prof) drain_profile(S);
+        if (!known) {
+            CK(cudaMemcpyAsync(S.h_counts, S.qs.count, sizeof(unsigned) * 8, cudaMemcpyDeviceToHost, S.stream));
+            if (pending_trace)
+                CK(cudaMemcpyAsync(S.h_trace_chk, S.trace_chk, sizeof(ull), cudaMemcpyDeviceToHost, S.stream));
+            CK(cudaStreamSynchronize(S.stream));
+            if (prof) drain_profile(S);
+            if (check_prediction && std::memcmp(predicted, S.h_counts, sizeof predicted) != 0)
+                throw std::logic_error("queue-length prediction after a fuel calculate_xs launch was wrong");
+            check_prediction = false;
+        }
+        known = false;
         if (pending_trace) {
             S.trace.back() = (int64_t)S.h_trace_chk[0];
             pending_trace = false;
@@ -590,6 +604,16 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                         else launch_xs(c, qptr, n, true, S.stream);
                     }
                     if (prof) S.xs_fuel_bytes += (double)n * (44.0 + 100.0 * (double)fuel_nuc);
+                    if (predict && c.fused && !(dead > 0 && next < S.hi)) {
+                        S.h_counts[EV_ADV] += (unsigned)n;  // the move queue receives every entry
+                        S.h_counts[EV_XS_FUEL] = 0u;
+                        if (trace) {  // trace mode reads back anyway and checks the prediction
+                            std::memcpy(predicted, S.h_counts, sizeof predicted);
+                            check_prediction = true;
+                        } else {
+                            known = true;
+                        }
+                    }
                     break;
                 case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, false, S.stream); } break;
                 case EV_ADV: {
