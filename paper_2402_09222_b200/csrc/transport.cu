@@ -508,9 +508,11 @@ bool tail_warp() {
 void drain_profile(SubBank& S) {
     if (S.n_pending == 0) return;
     CK(cudaEventSynchronize(S.evs[S.n_pending - 1].b));
+    static const bool log = std::getenv("OMCG_PROF_LOG") != nullptr;  // per-launch lines to stderr
     for (int i = 0; i < S.n_pending; ++i) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, S.evs[i].a, S.evs[i].b));
+        if (log) std::fprintf(stderr, "[launch] class %d items %lld ms %.4f\n", S.evs[i].cls, (long long)S.evs[i].items, ms);
         S.prof_ms[S.evs[i].cls] += ms;
         S.prof_launches[S.evs[i].cls] += 1;
         S.prof_items[S.evs[i].cls] += S.evs[i].items;
