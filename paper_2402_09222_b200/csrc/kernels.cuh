@@ -59,11 +59,9 @@ void launch_tail(const Ctx& c, bool queued, int64_t live, int32_t* list, cudaStr
 void launch_refill_all(const Ctx& c, int64_t first_local, int64_t n_remaining, const Site* src,
                        cudaStream_t s);
 void launch_xs(const Ctx& c, const int32_t* q, int n, bool fuel, cudaStream_t s);
-// fuel-queue calculate_xs split by 16-nuclide segment (nseg segments, partial
-// sums in part[nseg][4][cap]) + an in-order fold; same arithmetic as launch_xs
-void launch_xs_fuel_split(const Ctx& c, const int32_t* q, int n, int nseg, double* part, cudaStream_t s);
-// the same split lookup in one launch: a block per 32 entries, segment
-// partials in shared memory, in-order fold by warp 0 (nseg <= 48)
+// fuel-queue calculate_xs split by 16-nuclide segment in one launch: a block
+// per 32 entries, segment partials in shared memory, in-order fold by warp 0
+// (nseg <= 48); same arithmetic as launch_xs
 void launch_xs_fuel_fused(const Ctx& c, const int32_t* q, int n, int nseg, cudaStream_t s);
 void launch_advance(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 void launch_cross(const Ctx& c, const int32_t* q, int n, cudaStream_t s);

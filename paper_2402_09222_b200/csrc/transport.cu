@@ -266,7 +266,6 @@ struct SubBank {
     Bank b{};
     QueueSet qs{};
     int32_t* q_sorted = nullptr;
-    double* part = nullptr;  // split fuel calculate_xs partial sums [seg][4][cap]
     int32_t* tail_list = nullptr;  // live slots for the warp-per-history tail
     uint32_t* keys = nullptr;
     unsigned* hist = nullptr;
@@ -431,7 +430,6 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
             S.dead_head = 0;
         }
         S.q_sorted = A.alloc<int32_t>(cap);
-        if (xs_fuel_mode() == 1) S.part = A.alloc<double>((int64_t)R.gp.max_fuel_seg * 4 * cap);
         S.tail_list = A.alloc<int32_t>(cap);
         S.keys = A.alloc<uint32_t>(cap);
         S.hist = A.alloc<unsigned>((int64_t)R.gp.n_fuel_mats * 65536);
@@ -485,16 +483,16 @@ void teardown_rank(Rank& R) {
 }
 
 // ------------------------------------------------------------------ event loops
-// A/B switches: OMCG_XS_SPLIT / OMCG_XS_FUSED select the fuel lookup
-// variant, OMCG_TAIL_WARP=0 the thread-per-history tail.
+// A/B switches: OMCG_XS_SPLIT=0 selects the one-history-per-thread fuel
+// lookup, OMCG_TAIL_WARP=0 the thread-per-history tail.
 bool env_flag(const char* name) {
     const char* v = std::getenv(name);
     return !v || std::atoi(v) != 0;
 }
-// fuel calculate_xs variant: 2 fused split (default), 1 two-launch split
-// (OMCG_XS_FUSED=0), 0 one history per thread (OMCG_XS_SPLIT=0)
+// fuel calculate_xs variant: 2 split by segment in one launch (default), 0 one
+// history per thread (OMCG_XS_SPLIT=0)
 int xs_fuel_mode() {
-    static const int m = !env_flag("OMCG_XS_SPLIT") ? 0 : !env_flag("OMCG_XS_FUSED") ? 1 : 2;
+    static const int m = !env_flag("OMCG_XS_SPLIT") ? 0 : 2;
     return m;
 }
 bool tail_warp() {
@@ -611,7 +609,6 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                         Prof pf(S, prof, 0, n);
                         const int xm = xs_fuel_mode();
                         if (xm == 2) launch_xs_fuel_fused(c, qptr, n, R.gp.max_fuel_seg, S.stream);
-                        else if (xm == 1) launch_xs_fuel_split(c, qptr, n, R.gp.max_fuel_seg, S.part, S.stream);
                         else launch_xs(c, qptr, n, true, S.stream);
                     }
                     if (prof) S.xs_fuel_bytes += (double)n * (44.0 + 100.0 * (double)fuel_nuc);
