@@ -1108,9 +1108,11 @@ static void transport(const orc_problem* p, particle* q, accum* A, double k_norm
  * tail_threshold histories are alive, all of them are finished at once
  * (recorded as queue 5). Trace entries: (queue, length, sum of mix64(id+1)).
  * event_fusion (the product's default, omcg_run_config.event_fusion): the
- * advance queue is the "move" queue — each of its histories runs events back
- * to back until it needs a calculate_xs in a fissionable (fuel) material,
- * collides in one, or dies; non-fuel lookups of new histories join it too. */
+ * advance queue is the "move" queue — each of its histories runs flights,
+ * surface crossings and non-fuel calculate_xs back to back until it needs a
+ * calculate_xs in a fissionable (fuel) material, collides, or dies; every
+ * non-fuel lookup (after a non-fuel collision, or of a new history) is done in
+ * the move queue. */
 enum { Q_XS_FUEL = 0, Q_XS_NONFUEL = 1, Q_ADV = 2, Q_CROSS = 3, Q_COLL = 4, Q_DEAD = 5 };
 
 static uint64_t mix64(uint64_t z) {
@@ -1125,6 +1127,8 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
     int64_t cap = in_flight < n_particles ? in_flight : n_particles;
     particle* slots = (particle*)malloc(sizeof(particle) * (size_t)cap);
     int* ev = (int*)malloc(sizeof(int) * (size_t)cap);
+    int* pend = (int*)malloc(sizeof(int) * (size_t)cap); /* pending event of each slot (the move
+                                                              queue holds flights and non-fuel lookups) */
     /* per-slot cross-section cache: energy of the last lookup of each material,
      * and the last many-nuclide (> SEG_LEN) material looked up (whose segment
      * checkpoints the product keeps) */
@@ -1133,8 +1137,8 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
     accum A;
     memset(&A, 0, sizeof A);
     A.tally = (int64_t*)calloc(4 * (size_t)p->geo.nx * (size_t)p->geo.ny, sizeof(int64_t));
-    if (!slots || !ev || !A.tally || !cache_E || !cache_m) {
-        free(slots); free(ev); free(A.tally); free(cache_E); free(cache_m);
+    if (!slots || !ev || !pend || !A.tally || !cache_E || !cache_m) {
+        free(slots); free(ev); free(pend); free(A.tally); free(cache_E); free(cache_m);
         return fail("out of memory");
     }
     for (int64_t s = 0; s < cap; ++s) ev[s] = Q_DEAD;
@@ -1157,7 +1161,7 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
                 if (ev[s] == Q_DEAD || (!tail && ev[s] != best)) continue;
                 particle* q = &slots[s];
                 chk += mix64((uint64_t)q->gidx + 1ULL);
-                int e = ev[s] <= Q_XS_NONFUEL ? EV_XS : ev[s] == Q_ADV ? EV_ADV : ev[s] == Q_CROSS ? EV_CROSS : EV_COLL;
+                int e = pend[s];
                 do {  /* one event, or the whole remainder in the tail */
                     const int prev = e;
                     switch (e) {
@@ -1179,8 +1183,10 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
                         (p->mat[q->mat].n <= SEG_LEN || cache_m[s] == q->mat))
                         e = ev_xs(p, q);
                 } while (e != EV_DEAD &&
-                         (tail || (move && !((e == EV_XS || e == EV_COLL) && p->mat[q->mat].fissionable))));
-                ev[s] = e == EV_DEAD ? Q_DEAD : e == EV_XS ? (p->mat[q->mat].fissionable ? Q_XS_FUEL : Q_XS_NONFUEL)
+                         (tail || (move && !((e == EV_XS && p->mat[q->mat].fissionable) || e == EV_COLL))));
+                pend[s] = e;
+                ev[s] = e == EV_DEAD ? Q_DEAD
+                        : e == EV_XS ? (p->mat[q->mat].fissionable ? Q_XS_FUEL : event_fusion ? Q_ADV : Q_XS_NONFUEL)
                         : e == EV_ADV ? Q_ADV : e == EV_CROSS ? Q_CROSS : Q_COLL;
             }
             if (out && n < max_entries) {
@@ -1199,6 +1205,7 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
                 cache_E[3 * s] = cache_E[3 * s + 1] = cache_E[3 * s + 2] = -1.0;
                 cache_m[s] = -1;
                 ev[s] = p->mat[slots[s].mat].fissionable ? Q_XS_FUEL : event_fusion ? Q_ADV : Q_XS_NONFUEL;
+                pend[s] = EV_XS;
                 next++;
                 k--;
             }
@@ -1206,7 +1213,7 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
         }
     }
     *n_out = n;
-    free(slots); free(ev); free(A.tally); free(A.bank); free(cache_E); free(cache_m);
+    free(slots); free(ev); free(pend); free(A.tally); free(A.bank); free(cache_E); free(cache_m);
     return rc;
 }
 
