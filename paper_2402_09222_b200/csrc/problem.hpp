@@ -8,6 +8,8 @@
 // Buffers live in host memory; omcg_run uploads them (the e2e path).
 #pragma once
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -41,6 +43,21 @@ struct Problem {
     Geometry geo{};                 // pin_map points into pin_map_host
     std::vector<uint8_t> pin_map_host;
     double gen_seconds = 0.0;       // library generation wall time
+    // E / xs page-locked on first upload (cudaHostRegister), released with the
+    // problem (or when it is reassigned): later uploads copy at full rate
+    struct Pins {
+        std::mutex mu;
+        std::shared_ptr<void> E, xs;
+        Pins() = default;
+        Pins(const Pins&) {}
+        Pins& operator=(const Pins&) {
+            std::lock_guard<std::mutex> lk(mu);
+            E.reset();
+            xs.reset();
+            return *this;
+        }
+    };
+    mutable Pins pins;
 
     int64_t grid_points() const { return goff.empty() ? 0 : goff.back(); }
     int64_t library_bytes() const { return grid_points() * (int64_t)(sizeof(double) + sizeof(XS4)); }

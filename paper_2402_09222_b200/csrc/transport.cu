@@ -135,6 +135,8 @@ struct DevArena {
     }
 };
 
+bool env_flag(const char* name);  // unset or nonzero -> true
+
 // Library + hash grid + geometry resident in one GPU's HBM.
 struct GpuProblem {
     DevArena arena;
@@ -203,6 +205,20 @@ struct GpuProblem {
         for (size_t i = 0; i < mnuc.size(); ++i) {
             int n = mnuc[i];
             mdesc[i] = make_int4(goff[n], goff[n + 1] - goff[n], n * (n_bins + 1), n);
+        }
+        static const bool pin_lib = env_flag("OMCG_PIN_LIBRARY");
+        if (pin_lib) {  // page-lock the two big host arrays once per problem (best effort)
+            std::lock_guard<std::mutex> lk(p.pins.mu);
+            auto pin = [](const void* ptr, size_t bytes, std::shared_ptr<void>& guard) {
+                if (guard || bytes == 0) return;
+                void* q = const_cast<void*>(ptr);
+                if (cudaHostRegister(q, bytes, cudaHostRegisterDefault) == cudaSuccess)
+                    guard.reset(q, [](void* r) { cudaHostUnregister(r); });
+                else
+                    cudaGetLastError();
+            };
+            pin(p.E.data(), sizeof(double) * p.E.size(), p.pins.E);
+            pin(p.xs.data(), sizeof(XS4) * p.xs.size(), p.pins.xs);
         }
         auto up = [&](auto* dst, const auto* src, size_t n) {
             size_t bytes = sizeof(*src) * n;
@@ -333,7 +349,6 @@ struct Rank {
     std::string error;
 };
 
-bool env_flag(const char* name);  // unset or nonzero -> true
 int xs_fuel_mode();
 
 // ------------------------------------------------------------------ setup
