@@ -72,7 +72,8 @@ void launch_collide(const Ctx& c, const int32_t* q, int n, int n_front, cudaStre
 // fused transport: every history of the move queue runs advance / crossing /
 // non-fuel calculate_xs / non-fuel collision in registers until it needs a
 // fuel lookup, collides in fuel or dies
-// coll_in: non-fuel collisions run inside the loop (queueless sweeps; end of batch)
+// coll_in: non-fuel collisions run inside the loop (always for the queueless
+// sweep; for the queued end of a batch it measured neutral, so it is unused there)
 void launch_move(const Ctx& c, const int32_t* q, int n, cudaStream_t s, bool coll_in = false);
 // diagnostic build only (-DOMCG_MOVE_CYCLES): per-event-type cycle shares of k_move to stderr
 void dump_move_cycles();

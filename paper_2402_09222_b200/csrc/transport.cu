@@ -641,9 +641,7 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                 case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, false, S.stream); } break;
                 case EV_ADV: {
                     Prof pf(S, prof, 2, n);
-                    static const int64_t collin_below =
-                        std::getenv("OMCG_MOVE_COLLIN_BELOW") ? std::atoll(std::getenv("OMCG_MOVE_COLLIN_BELOW")) : 0;
-                    if (c.fused) launch_move(c, qptr, n, S.stream, live <= collin_below);
+                    if (c.fused) launch_move(c, qptr, n, S.stream);
                     else launch_advance(c, qptr, n, S.stream);
                 } break;
                 case EV_CROSS: { Prof pf(S, prof, 3, n); launch_cross(c, qptr, n, S.stream); } break;
