@@ -54,7 +54,8 @@ struct alignas(128) PState {
     int32_t gidx;           // batch-global history index
     int8_t ring, mat, surf, pad0;
     int32_t n_sites;        // fission sites banked so far
-    int32_t pad1[2];
+    int32_t bin;            // log hash-grid bin of E (set whenever E changes: one det_log per energy)
+    int32_t pad1;
 };
 static_assert(sizeof(PState) == 128, "PState must be one 128-byte line");
 
