@@ -36,7 +36,7 @@ struct Ctx {
     uint64_t master;
     int64_t record_n;
     int recording;
-    unsigned long long* ctrl;  // [0] refill ticket, [1] alive, [2] error flags, [3] tail list, [4] move chunks
+    unsigned long long* ctrl;  // [0] refill ticket, [1] alive, [2] error flags, [3] tail list, [4] move chunks, [5] queueless lookup chunks
     int fused;                 // event fusion: non-fuel XS work goes to the move (advance) queue
 };
 
