@@ -105,6 +105,12 @@ typedef struct {
      * separate kernels (queued: separate queues; queueless: separate sweeps).
      * Results are identical either way. */
     int event_fusion;
+    /* Event fusion, queued mode: a history runs at most this many events
+     * (flights, crossings, non-fuel lookups) per move-kernel launch, then
+     * rejoins the move queue for the next one; this bounds the launch's tail
+     * of long flights through the moderator (default 20; 0: no cap). Results
+     * are identical for every value; only the queue contents change. */
+    int move_event_cap;
 } omcg_run_config;
 
 typedef struct {

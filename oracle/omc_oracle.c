@@ -1112,7 +1112,10 @@ static void transport(const orc_problem* p, particle* q, accum* A, double k_norm
  * surface crossings and non-fuel calculate_xs back to back until it needs a
  * calculate_xs in a fissionable (fuel) material, collides, or dies; every
  * non-fuel lookup (after a non-fuel collision, or of a new history) is done in
- * the move queue. */
+ * the move queue. move_cap > 0 (omcg_run_config.move_event_cap): a history
+ * leaves a move iteration after at most move_cap events (the cross-section
+ * cache hit that follows a crossing is part of the crossing) and stays in the
+ * move queue, whatever its next event. */
 enum { Q_XS_FUEL = 0, Q_XS_NONFUEL = 1, Q_ADV = 2, Q_CROSS = 3, Q_COLL = 4, Q_DEAD = 5 };
 
 static uint64_t mix64(uint64_t z) {
@@ -1122,7 +1125,8 @@ static uint64_t mix64(uint64_t z) {
 }
 
 int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, int64_t in_flight,
-                    int64_t tail_threshold, int event_fusion, int64_t* out, int64_t max_entries, int64_t* n_out) {
+                    int64_t tail_threshold, int event_fusion, int move_cap, int64_t* out, int64_t max_entries,
+                    int64_t* n_out) {
     if (!p || !n_out || n_particles < 1 || in_flight < 1) return fail("invalid queue-trace arguments");
     int64_t cap = in_flight < n_particles ? in_flight : n_particles;
     particle* slots = (particle*)malloc(sizeof(particle) * (size_t)cap);
@@ -1161,9 +1165,10 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
                 if (ev[s] == Q_DEAD || (!tail && ev[s] != best)) continue;
                 particle* q = &slots[s];
                 chk += mix64((uint64_t)q->gidx + 1ULL);
-                int e = pend[s];
+                int e = pend[s], steps = 0;
                 do {  /* one event, or the whole remainder in the tail */
                     const int prev = e;
+                    steps++;
                     switch (e) {
                     case EV_XS: e = ev_xs(p, q); break;
                     case EV_ADV: e = ev_advance(p, q, &A); break;
@@ -1183,11 +1188,12 @@ int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, in
                         (p->mat[q->mat].n <= SEG_LEN || cache_m[s] == q->mat))
                         e = ev_xs(p, q);
                 } while (e != EV_DEAD &&
-                         (tail || (move && !((e == EV_XS && p->mat[q->mat].fissionable) || e == EV_COLL))));
+                         (tail || (move && !((e == EV_XS && p->mat[q->mat].fissionable) || e == EV_COLL) &&
+                                   !(move_cap > 0 && steps >= move_cap))));
                 pend[s] = e;
                 ev[s] = e == EV_DEAD ? Q_DEAD
                         : e == EV_XS ? (p->mat[q->mat].fissionable ? Q_XS_FUEL : event_fusion ? Q_ADV : Q_XS_NONFUEL)
-                        : e == EV_ADV ? Q_ADV : e == EV_CROSS ? Q_CROSS : Q_COLL;
+                        : e == EV_ADV ? Q_ADV : e == EV_CROSS ? (event_fusion ? Q_ADV : Q_CROSS) : Q_COLL;
             }
             if (out && n < max_entries) {
                 out[3 * n] = tail ? Q_DEAD : best;

@@ -120,7 +120,8 @@ int orc_run(const orc_problem* p, const orc_run_config* cfg, orc_run_result* res
  * source): per iteration (queue id, length, sum of mix64(history+1)); queue 5
  * = tail (all live histories finished at once). Mirrors omcg_queue_trace. */
 int orc_queue_trace(const orc_problem* p, int64_t n_particles, uint64_t seed, int64_t in_flight,
-                    int64_t tail_threshold, int event_fusion, int64_t* out, int64_t max_entries, int64_t* n_out);
+                    int64_t tail_threshold, int event_fusion, int move_cap, int64_t* out, int64_t max_entries,
+                    int64_t* n_out);
 
 const char* orc_last_error(void);
 

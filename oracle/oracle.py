@@ -96,7 +96,7 @@ def lib() -> C.CDLL:
         L.orc_particle_seed.restype = C.c_uint64
         L.orc_run.argtypes = [P, C.POINTER(RunConfig), C.POINTER(RunResult), C.c_void_p, C.c_void_p]
         L.orc_last_error.restype = C.c_char_p
-        L.orc_queue_trace.argtypes = [P, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_void_p,
+        L.orc_queue_trace.argtypes = [P, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_void_p,
                                       C.c_int64, C.POINTER(C.c_int64)]
         _lib = L
     return _lib
@@ -150,16 +150,18 @@ class Problem:
         return E, xs
 
     def queue_trace(self, n_particles: int, in_flight: int, tail_threshold: int, seed: int = 1,
-                    event_fusion: bool = True):
-        """Queued event-loop emulation of batch 1: array of (queue, length, id-checksum)."""
+                    event_fusion: bool = True, move_cap: int = 20):
+        """Queued event-loop emulation of batch 1: array of (queue, length, id-checksum).
+        move_cap mirrors omcg_run_config.move_event_cap (used with event fusion only)."""
         import numpy as np
         n = C.c_int64()
         f = int(bool(event_fusion))
-        if lib().orc_queue_trace(self._p, n_particles, seed, in_flight, tail_threshold, f, None, 0, C.byref(n)) != 0:
+        if lib().orc_queue_trace(self._p, n_particles, seed, in_flight, tail_threshold, f, move_cap, None, 0,
+                                 C.byref(n)) != 0:
             raise RuntimeError(lib().orc_last_error().decode())
         out = np.zeros((n.value, 3), np.int64)
-        lib().orc_queue_trace(self._p, n_particles, seed, in_flight, tail_threshold, f, out.ctypes.data, n.value,
-                              C.byref(n))
+        lib().orc_queue_trace(self._p, n_particles, seed, in_flight, tail_threshold, f, move_cap, out.ctypes.data,
+                              n.value, C.byref(n))
         return out
 
     def run(self, n_particles: int, n_batches: int, n_inactive: int, seed: int = 1, threads: int = 0,

@@ -106,7 +106,7 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
                 host_threads=8, tasks_per_gpu=1, cpu_bind="threads", n_particles=1_000_000,
                 n_batches=15, n_inactive=5, seed=1, n_gpus=1, devices=None, world_size=1, rank=0,
                 nccl_id: bytes | None = None, record_batch=0, record_n=0, profile=False,
-                trace_queues=False, tail_threshold=None, event_fusion=None) -> RunConfig:
+                trace_queues=False, tail_threshold=None, event_fusion=None, move_event_cap=None) -> RunConfig:
     cfg = RunConfig()
     _lib.omcg_run_config_default(C.byref(cfg))
     m = {"openmc": QUEUED, "queued": QUEUED, "openmc-queueless": QUEUELESS,
@@ -140,6 +140,8 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
         cfg.tail_threshold = int(tail_threshold)
     if event_fusion is not None:
         cfg.event_fusion = int(event_fusion)
+    if move_event_cap is not None:
+        cfg.move_event_cap = int(move_event_cap)
     return cfg
 
 

@@ -45,7 +45,7 @@ class RunConfig(C.Structure):
         ("devices", C.c_int * 8), ("world_size", C.c_int), ("rank", C.c_int),
         ("nccl_id", C.c_ubyte * 128), ("record_batch", C.c_int), ("record_n", C.c_int64),
         ("profile", C.c_int), ("trace_queues", C.c_int), ("tail_threshold", C.c_int64),
-        ("event_fusion", C.c_int),
+        ("event_fusion", C.c_int), ("move_event_cap", C.c_int),
     ]
 
 

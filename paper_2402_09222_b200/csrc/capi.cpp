@@ -131,6 +131,7 @@ OMCG_API void omcg_run_config_default(omcg_run_config* c) {
     c->rank = 0;
     c->tail_threshold = 16384;
     c->event_fusion = 1;
+    c->move_event_cap = 20;
 }
 
 OMCG_API int omcg_run(const omcg_problem* p, const omcg_run_config* cfg, omcg_run_result* res, int64_t* tally_out,

@@ -14,7 +14,9 @@ struct QueueSet {
     int64_t cap;
     unsigned* count;
     unsigned long long* dead_tail;
+    int adv_q;  // region receiving move-queue (EV_ADV) appends: EV_ADV or ADV_ALT (flips per capped move launch)
 };
+constexpr int ADV_ALT = 6;  // the second move-queue region (N_QUEUES + 1 regions are allocated)
 
 // Everything an event kernel needs, passed by value as the kernel parameter.
 struct Ctx {
@@ -38,6 +40,7 @@ struct Ctx {
     int recording;
     unsigned long long* ctrl;  // [0] refill ticket, [1] alive, [2] error flags, [3] tail list, [4] move chunks, [5] queueless lookup chunks
     int fused;                 // event fusion: non-fuel XS work goes to the move (advance) queue
+    int move_cap;              // > 0: a history runs at most move_cap events per move launch, then rejoins the move queue
 };
 
 constexpr int SMEM_TALLY_MAX = 64;  // tally bins*scores aggregated per block in smem (few-pin problems)

@@ -132,6 +132,7 @@ int main(int argc, char** argv) {
     cfg.n_inactive = (int)env_ll("OMCG_INACTIVE", cfg.n_inactive);
     cfg.seed = (uint64_t)env_ll("OMCG_SEED", 1);
     cfg.event_fusion = (int)env_ll("OMCG_EVENT_FUSION", cfg.event_fusion);
+    cfg.move_event_cap = (int)env_ll("OMCG_MOVE_CAP", cfg.move_event_cap);
     const uint64_t xs_seed = (uint64_t)env_ll("OMCG_XS_SEED", 1234);
     const int want = (int)env_ll("OMCG_GPUS", 1);
     bind_cpus(cfg.cpu_bind, cfg.host_threads);

@@ -430,7 +430,8 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         B.ckpt = A.alloc<double>((int64_t)NCKPT * cap);
         CK(cudaMemsetAsync(B.event, EV_DEAD, (size_t)cap, S.stream));
         S.qs.cap = cap;
-        S.qs.qbase = A.alloc<int32_t>((int64_t)N_QUEUES * cap);
+        S.qs.qbase = A.alloc<int32_t>((int64_t)(N_QUEUES + 1) * cap);  // + the second move-queue region
+        S.qs.adv_q = EV_ADV;
         S.qs.count = A.alloc<unsigned>(8);  // [0..4] live lengths, [6..7] dead tail (u64)
         S.qs.dead_tail = reinterpret_cast<ull*>(S.qs.count + 6);
         {   // every slot starts in the dead ring
@@ -610,7 +611,7 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                 launch_tail(c, true, live, tail_warp() ? S.tail_list : nullptr, S.stream);
                 S.tail_launches++;
             } else {
-                const int32_t* qptr = S.qs.qbase + (int64_t)best * S.qs.cap;
+                const int32_t* qptr = S.qs.qbase + (int64_t)(best == EV_ADV ? c.qs.adv_q : best) * S.qs.cap;
                 switch (best) {
                 case EV_XS_FUEL:
                     if (cfg.sort_threshold >= 0 && n >= cfg.sort_threshold) {
@@ -641,6 +642,10 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                 case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, false, S.stream); } break;
                 case EV_ADV: {
                     Prof pf(S, prof, 2, n);
+                    if (c.fused && c.move_cap) {  // capped histories go to the other region
+                        c.qs.adv_q = c.qs.adv_q == EV_ADV ? ADV_ALT : EV_ADV;
+                        CK(cudaMemsetAsync(S.qs.count + EV_ADV, 0, sizeof(unsigned), S.stream));
+                    }
                     if (c.fused) launch_move(c, qptr, n, S.stream);
                     else launch_advance(c, qptr, n, S.stream);
                 } break;
@@ -879,6 +884,9 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         base.record_n = cfg.record_n;
         base.recording = (R.acc.records && batch == cfg.record_batch) ? 1 : 0;
         base.fused = cfg.event_fusion ? 1 : 0;
+        base.move_cap = cfg.event_fusion ? std::max(0, cfg.move_event_cap) : 0;
+        if (cfg.event_fusion && std::getenv("OMCG_MOVE_CAP_AB"))  // A/B override (scripts/ab.sh)
+            base.move_cap = std::atoi(std::getenv("OMCG_MOVE_CAP_AB"));
         const Site* src = have_source ? R.source : nullptr;
         const bool prof = cfg.profile != 0 && active;
 

@@ -1,7 +1,7 @@
 # A/B of env switches on the C2 bench (short: 2 inactive + 5 active batches).
 # usage: bash scripts/ab.sh "ENV=.. ENV2=.." "ENV=.." ...   (BENCH_ARGS: extra bench.py flags)
 for v in "$@"; do
-  r=$(env $v timeout 600 python bench.py --steps 5 --warmup 2 --no-cpu-baseline $BENCH_ARGS 2>/dev/null | tail -1)
+  r=$(env $v timeout 600 python bench.py ${BENCH_ARGS:---steps 5 --warmup 2} --no-cpu-baseline 2>/dev/null | tail -1)
   python - "$v" "$r" <<'PY'
 import json,sys
 try:

@@ -174,3 +174,11 @@ def test_queue_trace_consistent_with_history_transport(kind):
     assert int(t1[t1[:, 0] == 4, 1].sum()) <= res.n_events[3]
     # every history enters the move queue at least once; id checksums are order-free sums
     assert int(t1[t1[:, 0] == 2, 1].sum()) >= n
+    # move-kernel event cap: 1 -> every flight and every crossing takes its own
+    # move-queue entry; a cap no history reaches -> the uncapped trace
+    t_c1 = p.queue_trace(n, n, 0, seed=1, event_fusion=True, move_cap=1)
+    assert int(t_c1[t_c1[:, 0] == 2, 1].sum()) >= res.n_events[1] + res.n_events[2]
+    assert set(np.unique(t_c1[:, 0])) <= {0, 2, 4}
+    t_off = p.queue_trace(n, n, 0, seed=1, event_fusion=True, move_cap=0)
+    assert np.array_equal(p.queue_trace(n, n, 0, seed=1, event_fusion=True, move_cap=10**6), t_off)
+    assert len(t_c1) > len(t_off)
