@@ -85,15 +85,27 @@ class ClockSampler:
         except OSError:
             self.p = None
 
+    def mark(self):
+        """Start of the timed region: samples written before it are dropped (the
+        sampler is started earlier so that nvidia-smi's own start-up, which takes
+        driver locks, does not fall inside the timed region)."""
+        if self.p is not None:
+            self.f.flush()
+            self.offset = os.path.getsize(self.f.name)
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
         self.p.wait()
         self.f.seek(0)
+        text = self.f.read()
+        timed = text[getattr(self, "offset", 0):]
+        if sum(1 for ln in timed.splitlines() if ln.count(",") >= 8) >= 2:
+            text = timed
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().splitlines():
+        for line in text.splitlines():
             c = [x.strip() for x in line.split(",")]
             if len(c) < 9:
                 continue
@@ -192,6 +204,7 @@ def main():
         obj = [(P.nccl_unique_id(), P.nccl_unique_id()) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         warm_id, nccl_id = obj[0]
+    sampler = ClockSampler() if rank == 0 else None
     # untimed warm-up call of the same configuration (one batch): loads the
     # kernels (lazy module loading) and lets the device memory pool reach its
     # working size, so the timed call measures a warm process, as a
@@ -200,10 +213,11 @@ def main():
           sort_threshold=a.sort if a.mode == "openmc" else None, host_threads=8, tasks_per_gpu=a.tasks,
           n_particles=a.particles * world, n_batches=1, n_inactive=0, seed=7, world_size=world, rank=rank,
           nccl_id=warm_id, devices=[local], event_fusion=a.event_fusion, tail_threshold=a.tail)
-    sampler = ClockSampler() if rank == 0 else None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    if sampler:
+        sampler.mark()
     t0 = time.perf_counter()
     out = P.run(problem, mode=a.mode, particles_in_flight=a.in_flight, n_bins=a.bins,
                 sort_threshold=a.sort if a.mode == "openmc" else None, host_threads=8, tasks_per_gpu=a.tasks,
@@ -212,6 +226,7 @@ def main():
                 event_fusion=a.event_fusion, tail_threshold=a.tail)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    clocks = sampler.stop() if sampler else None
     # short separately-profiled pass (every kernel class timed) for the kernel shares only
     shares = None
     if world == 1:
@@ -228,7 +243,6 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wall = float(t.item())
         dist.barrier()
-    clocks = sampler.stop() if sampler else None
     r = out.result
     if rank != 0:
         dist.destroy_process_group()
