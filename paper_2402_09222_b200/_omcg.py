@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libomcg.so")
+LIB_PATH = os.environ.get("OMCG_LIB_AB") or os.path.join(_HERE, "libomcg.so")  # (A/B builds only)
 
 OMCG_OK, OMCG_EINVAL, OMCG_EIO, OMCG_ECUDA, OMCG_ENCCL, OMCG_EFAIL = range(6)
 PINCELL, ASSEMBLY, CORE = 0, 1, 2

@@ -1,0 +1,3 @@
+export BENCH_ARGS="--steps 10 --warmup 3"
+bash scripts/ab.sh "OMCG_X=0" "OMCG_LIB_AB=$PWD/ab_libs/libomcg_div.so" "OMCG_X=0" "OMCG_LIB_AB=$PWD/ab_libs/libomcg_div.so"
+OMCG_LIB_AB=$PWD/ab_libs/libomcg_div.so timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
