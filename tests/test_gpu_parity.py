@@ -117,7 +117,29 @@ def test_queue_contents_bit_exact(kind, n, in_flight, tail, sort, fusion, cap):
     # with ranks sharing GPU 0 through the in-process loopback transport
     dict(particles_in_flight=5000, n_gpus=2, devices=[0, 0]),
     dict(particles_in_flight=2000, n_gpus=3, devices=[0, 0, 0], tasks_per_gpu=2),
+    # move-kernel event cap: every event of the move queue a separate visit; no cap
+    dict(particles_in_flight=5000, tail_threshold=0, move_event_cap=1),
+    dict(particles_in_flight=5000, tail_threshold=0, move_event_cap=0),
+    # one history in flight at a time; more slots than histories
+    dict(particles_in_flight=1, tail_threshold=0),
+    dict(particles_in_flight=50000),
 ])
 def test_tuned_parameters_do_not_change_results(kw):
     """in-flight count (and every other tuned knob) changes time only."""
     _compare_runs(P.PINCELL, 10000, 3, 1, 1000, **kw)
+
+
+def test_core_transport_bit_exact():
+    """C4 geometry (37 assemblies, water reflector, vacuum boundaries: leakage)."""
+    out = _compare_runs(P.CORE, 3000, 2, 1, 500, particles_in_flight=3000, tail_threshold=100)
+    assert out.result.n_leaked > 0
+
+
+@pytest.mark.parametrize("kw", [
+    dict(n_gpus=3, devices=[0, 0, 0], tasks_per_gpu=4),   # ragged: 7 histories over 12 sub-banks
+    dict(particles_in_flight=2),
+    dict(mode="openmc-queueless", particles_in_flight=3),
+])
+def test_tiny_ragged_runs_bit_exact(kw):
+    """Edge sizes: fewer histories than ranks x sub-banks, a 2-slot bank."""
+    _compare_runs(P.PINCELL, 7, 3, 1, 7, **kw)
