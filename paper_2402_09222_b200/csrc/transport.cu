@@ -642,10 +642,8 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                 case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, false, S.stream); } break;
                 case EV_ADV: {
                     Prof pf(S, prof, 2, n);
-                    if (c.fused && c.move_cap) {  // capped histories go to the other region
+                    if (c.fused && c.move_cap)  // capped histories go to the other region
                         c.qs.adv_q = c.qs.adv_q == EV_ADV ? ADV_ALT : EV_ADV;
-                        CK(cudaMemsetAsync(S.qs.count + EV_ADV, 0, sizeof(unsigned), S.stream));
-                    }
                     if (c.fused) launch_move(c, qptr, n, S.stream);
                     else launch_advance(c, qptr, n, S.stream);
                 } break;
