@@ -85,6 +85,16 @@ class ClockSampler:
         except OSError:
             self.p = None
 
+    def wait_ready(self, timeout=5.0):
+        """Block until nvidia-smi has written its first sample (its start-up can
+        take a second or more and must not overlap the timed region)."""
+        t_end = time.time() + timeout
+        while self.p is not None and time.time() < t_end:
+            self.f.flush()
+            if os.path.getsize(self.f.name) > 0:
+                return
+            time.sleep(0.05)
+
     def mark(self):
         """Start of the timed region: samples written before it are dropped (the
         sampler is started earlier so that nvidia-smi's own start-up, which takes
@@ -217,6 +227,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     if sampler:
+        sampler.wait_ready()
         sampler.mark()
     t0 = time.perf_counter()
     out = P.run(problem, mode=a.mode, particles_in_flight=a.in_flight, n_bins=a.bins,
