@@ -66,9 +66,11 @@ class Problem:
         _check(_lib.omcg_problem_get_info(self._p, C.byref(self.info)))
         self.kind = k
 
-    def __del__(self):
+    def __del__(self, _free=_lib.omcg_problem_free):
+        # (the library function is bound at definition time: module globals may
+        # already be cleared when this runs at interpreter shutdown)
         if getattr(self, "_p", None):
-            _lib.omcg_problem_free(self._p)
+            _free(self._p)
             self._p = None
 
     @property
