@@ -33,3 +33,17 @@ def test_reference_arm_json_line():
 
 def test_reference_arm_other_ranks_silent():
     assert _run({"RANK": "1", "WORLD_SIZE": "2"}) == []
+
+
+def test_clock_sampler_degrades_without_a_gpu():
+    """The clocks key is always a dict with the contract's fields; on a host
+    without NVML / nvidia-smi it says so instead of failing the bench."""
+    sys.path.insert(0, ROOT)
+    import bench
+    s = bench.clock_sampler(0)
+    s.wait_ready(timeout=0.2)
+    s.mark()
+    d = s.stop()
+    for k in ("sm_mhz", "sm_max_mhz", "reasons"):
+        assert k in d, k
+    assert isinstance(d["reasons"], list)
