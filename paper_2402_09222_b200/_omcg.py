@@ -10,7 +10,12 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("OMCG_LIB_AB") or os.path.join(_HERE, "libomcg.so")  # (A/B builds only)
+LIB_PATH = os.path.join(_HERE, "libomcg.so")
+# A/B of compile-time variants on one GPU box: another build of this library
+# (a file named libomcg*.so) may be selected with OMCG_LIB_AB
+_ab = os.environ.get("OMCG_LIB_AB")
+if _ab and os.path.basename(_ab).startswith("libomcg") and _ab.endswith(".so"):
+    LIB_PATH = _ab
 
 OMCG_OK, OMCG_EINVAL, OMCG_EIO, OMCG_ECUDA, OMCG_ENCCL, OMCG_EFAIL = range(6)
 PINCELL, ASSEMBLY, CORE = 0, 1, 2
