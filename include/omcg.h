@@ -46,7 +46,10 @@ enum {
     OMCG_EFAIL = 5   /* unexpected internal failure */
 };
 
-enum { OMCG_PINCELL = 0, OMCG_ASSEMBLY = 1, OMCG_CORE = 2 };
+/* problem kinds: C1 pin cell, C2 17x17 assembly, C4 full core,
+ * and an analytic infinite homogeneous medium of one energy-independent
+ * nuclide (k_inf = nu*Sigma_f/Sigma_a = 1.5625) */
+enum { OMCG_PINCELL = 0, OMCG_ASSEMBLY = 1, OMCG_CORE = 2, OMCG_INFINITE = 3 };
 enum { OMCG_QUEUED = 0, OMCG_QUEUELESS = 1 };           /* P0 */
 enum { OMCG_BIND_CORES = 0, OMCG_BIND_THREADS = 1, OMCG_BIND_SOCKETS = 2 }; /* P6 */
 enum { OMCG_N_SCORES = 4 };   /* per pin: flux, absorption, fission, nu-fission */
@@ -111,6 +114,13 @@ typedef struct {
      * of long flights through the moderator (default 20; 0: no cap). Results
      * are identical for every value; only the queue contents change. */
     int move_event_cap;
+    /* 1: the per-batch exchanges (int64 tally/k all-reduce, bank-size
+     * all-gather, fission-bank send/recv) go through NCCL even when this
+     * process runs a single rank (a one-rank communicator), so the multi-GPU
+     * data plane runs on one GPU. 0 (default): NCCL only between ranks on
+     * different GPUs. Communicators are created once per placement and reused
+     * by later calls in the same process. */
+    int force_nccl;
 } omcg_run_config;
 
 typedef struct {
@@ -164,6 +174,18 @@ OMCG_API int omcg_hash_build(const omcg_problem* p, int n_bins, int device, uint
  * out = 4n doubles (total, absorption, fission, nu-fission). */
 OMCG_API int omcg_xs_lookup(const omcg_problem* p, int n_bins, int device, int64_t n,
                             const int32_t* mat, const double* E, double* out);
+
+/* The production fuel lookup (calculate_xs kernel k_xs_fuel_fused, the one
+ * the queued loop launches) on a queue of n histories at (mat[i], E[i]),
+ * queue entry i = history i; the queue is first sorted by (material, energy)
+ * when n >= sort_threshold >= 0, as the queued loop does (P3). out: 4n doubles
+ * (total, absorption, fission, nu-fission) as stored in each record;
+ * ckpt_out (optional, 16n doubles): per history the folded running total
+ * after each 16-nuclide segment but the last (the collision's sampling
+ * checkpoints), unused entries NaN. Fails (OMCG_EFAIL) if the launch does not
+ * hand every history on to the move queue exactly once. */
+OMCG_API int omcg_xs_lookup_queue(const omcg_problem* p, int n_bins, int device, int64_t n, const int32_t* mat,
+                                  const double* E, int64_t sort_threshold, double* out, double* ckpt_out);
 
 /* ---- the transport run (the `openmc --event` body) ---- */
 OMCG_API void omcg_run_config_default(omcg_run_config* cfg);

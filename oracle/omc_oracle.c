@@ -458,15 +458,100 @@ static int bin_of(const orc_problem* p, double E) {
     return b < p->n_bins ? b : p->n_bins - 1;
 }
 
+/* hash grid [P217]: hash[n][k] = last i with bin(E_i) < k (>= 0) */
+static int build_hash(orc_problem* p) {
+    const int n_bins = p->n_bins;
+    p->inv_spacing = (double)n_bins / LN_RANGE;
+    size_t hb = (size_t)(n_bins + 1);
+    p->hash = (int32_t*)malloc(sizeof(int32_t) * hb * (size_t)p->n_nuc);
+    if (!p->hash) return -1;
+    for (int n = 0; n < p->n_nuc; ++n) {
+        const nuclide* N = &p->nuc[n];
+        for (int k = 0; k <= n_bins; ++k) {
+            int lo = 0, hi = N->n - 1;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (bin_of(p, N->E[mid]) < k) lo = mid + 1;
+                else hi = mid;
+            }
+            p->hash[(size_t)n * hb + (size_t)k] = lo > 0 ? lo - 1 : 0;
+        }
+    }
+    return 0;
+}
+
+/* Analytic check problem (ORC_INFINITE): infinite homogeneous medium of one
+ * nuclide with energy-independent cross sections (1001-point log grid,
+ * density 1 atom/(b cm)), every region fuel, reflective 1.26 x 1.26 x 200 cm
+ * box. Exact expectations, independent of both code bases: k_inf =
+ * nu*Sigma_f/Sigma_a, every history absorbed, Sigma_t/Sigma_a collisions and
+ * 1/Sigma_a track length per history. */
+static int build_infinite(orc_problem* p) {
+    const int ng = ORC_INF_GRID;
+    p->n_nuc = 1;
+    p->nuc = (nuclide*)calloc(1, sizeof(nuclide));
+    p->global_id = (int*)malloc(sizeof(int));
+    if (!p->nuc || !p->global_id) return fail("out of memory");
+    p->global_id[0] = -1;
+    nuclide* N = &p->nuc[0];
+    N->n = ng;
+    N->awr = ORC_INF_AWR;
+    N->fissionable = 1;
+    N->E = (double*)malloc(sizeof(double) * (size_t)ng);
+    N->xs = (double*)malloc(sizeof(double) * 4 * (size_t)ng);
+    if (!N->E || !N->xs) return fail("out of memory");
+    for (int i = 0; i < ng; ++i) {
+        N->E[i] = E_MIN * orc_exp((double)i / (double)(ng - 1) * LN_RANGE);
+        N->xs[4 * i] = ORC_INF_SIGMA_T;
+        N->xs[4 * i + 1] = ORC_INF_SIGMA_A;
+        N->xs[4 * i + 2] = ORC_INF_SIGMA_F;
+        N->xs[4 * i + 3] = ORC_INF_NU * ORC_INF_SIGMA_F;
+    }
+    N->E[0] = E_MIN;
+    N->E[ng - 1] = E_MAX;
+    p->n_mat = 3;
+    for (int m = 0; m < 3; ++m) {
+        material* M = &p->mat[m];
+        M->n = 1;
+        M->nuc = (int*)malloc(sizeof(int));
+        M->dens = (double*)malloc(sizeof(double));
+        if (!M->nuc || !M->dens) return fail("out of memory");
+        M->nuc[0] = 0;
+        M->dens[0] = 1.0;
+        M->fissionable = 1;
+    }
+    if (build_hash(p) != 0) return fail("out of memory (hash)");
+    geometry* G = &p->geo;
+    const int all_fuel[1] = {MAT_FUEL};
+    for (int t = 0; t < 3; ++t) set_pin(&G->pt[t], 0, NULL, all_fuel);
+    G->pitch = 1.26;
+    G->nx = G->ny = 1;
+    G->bc_x = G->bc_y = G->bc_z = 1;
+    G->x0 = G->y0 = -0.63;
+    G->z_lo = -100.0;
+    G->z_hi = 100.0;
+    G->pin_map = (unsigned char*)calloc(1, 1);
+    if (!G->pin_map) return fail("out of memory");
+    return 0;
+}
+
 int orc_problem_create(int kind, uint64_t xs_seed, int n_bins, orc_problem** out) {
     pthread_once(&g_const_once, init_consts);
-    if (kind < ORC_PINCELL || kind > ORC_CORE) return fail("unknown problem kind");
+    if (kind < ORC_PINCELL || kind > ORC_INFINITE) return fail("unknown problem kind");
     if (n_bins < 1 || n_bins > 10000000) return fail("n_bins out of range");
     orc_problem* p = (orc_problem*)calloc(1, sizeof *p);
     if (!p) return fail("out of memory");
     p->kind = kind;
     p->n_bins = n_bins;
     p->xs_seed = xs_seed;
+    if (kind == ORC_INFINITE) {
+        if (build_infinite(p) != 0) {
+            orc_problem_free(p);
+            return -1;
+        }
+        *out = p;
+        return 0;
+    }
 
     /* material composition in global ids */
     int mg_n[3];
@@ -537,23 +622,7 @@ int orc_problem_create(int kind, uint64_t xs_seed, int n_bins, orc_problem** out
     free(fuel_g);
     free(fuel_d);
 
-    /* hash grid [P217]: hash[n][k] = last i with bin(E_i) < k (>= 0) */
-    p->inv_spacing = (double)n_bins / LN_RANGE;
-    size_t hb = (size_t)(n_bins + 1);
-    p->hash = (int32_t*)malloc(sizeof(int32_t) * hb * (size_t)p->n_nuc);
-    if (!p->hash) { orc_problem_free(p); return fail("out of memory (hash)"); }
-    for (int n = 0; n < p->n_nuc; ++n) {
-        const nuclide* N = &p->nuc[n];
-        for (int k = 0; k <= n_bins; ++k) {
-            int lo = 0, hi = N->n - 1;
-            while (lo < hi) {
-                int mid = (lo + hi) >> 1;
-                if (bin_of(p, N->E[mid]) < k) lo = mid + 1;
-                else hi = mid;
-            }
-            p->hash[(size_t)n * hb + (size_t)k] = lo > 0 ? lo - 1 : 0;
-        }
-    }
+    if (build_hash(p) != 0) { orc_problem_free(p); return fail("out of memory (hash)"); }
 
     /* geometry */
     geometry* G = &p->geo;
@@ -705,6 +774,46 @@ static void macro_xs(const orc_problem* p, int m, double E, double out[4]) {
         for (int c = 0; c < 4; ++c) acc[c] = acc[c] + seg[c];
     }
     for (int c = 0; c < 4; ++c) out[c] = acc[c];
+}
+
+/* macro_xs plus the folded running total after every segment but the last
+ * (at most ORC_MAX_CKPT): the checkpoints the GPU's calculate_xs stores for the
+ * collision's nuclide sampling (cum = folded earlier segments + running sum in
+ * the segment, the order the collision below follows). */
+#define ORC_MAX_CKPT 16
+int orc_macro_xs_ckpt(const orc_problem* p, int mat, double E, double xs[4], double* ck, int* nck) {
+    if (mat < 0 || mat >= p->n_mat) return fail("material out of range");
+    const material* M = &p->mat[mat];
+    int b = bin_of(p, E);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int k = 0;
+    for (int s0 = 0; s0 < M->n; s0 += SEG_LEN) {
+        double seg[4] = {0.0, 0.0, 0.0, 0.0};
+        int s1 = s0 + SEG_LEN < M->n ? s0 + SEG_LEN : M->n;
+        for (int q = s0; q < s1; ++q) {
+            int n = M->nuc[q];
+            double f;
+            int i = grid_index(p, n, E, b, &f);
+            const double* x = p->nuc[n].xs;
+            double d = M->dens[q];
+            for (int c = 0; c < 4; ++c) seg[c] = fma(d, interp(x, i, c, f), seg[c]);
+        }
+        for (int c = 0; c < 4; ++c) acc[c] = acc[c] + seg[c];
+        if (s1 < M->n && k < ORC_MAX_CKPT) ck[k++] = acc[0];
+    }
+    for (int c = 0; c < 4; ++c) xs[c] = acc[c];
+    *nck = k;
+    return 0;
+}
+
+int orc_macro_xs_ckpt_n(const orc_problem* p, int64_t n, const int32_t* mat, const double* E, double* xs,
+                        double* ck, int32_t* nck) {
+    for (int64_t i = 0; i < n; ++i) {
+        int k = 0;
+        if (orc_macro_xs_ckpt(p, mat[i], E[i], xs + 4 * i, ck + ORC_MAX_CKPT * i, &k) != 0) return -1;
+        nck[i] = k;
+    }
+    return 0;
 }
 
 int orc_hash_bin(const orc_problem* p, double E) { return bin_of(p, E); }

@@ -32,7 +32,15 @@
 extern "C" {
 #endif
 
-enum { ORC_PINCELL = 0, ORC_ASSEMBLY = 1, ORC_CORE = 2 };
+enum { ORC_PINCELL = 0, ORC_ASSEMBLY = 1, ORC_CORE = 2, ORC_INFINITE = 3 };
+/* ORC_INFINITE: analytic infinite medium, one energy-independent nuclide
+ * (k_inf = ORC_INF_NU * ORC_INF_SIGMA_F / ORC_INF_SIGMA_A = 1.5625) */
+#define ORC_INF_GRID 1001
+#define ORC_INF_AWR 12.0
+#define ORC_INF_SIGMA_T 1.0
+#define ORC_INF_SIGMA_A 0.4
+#define ORC_INF_SIGMA_F 0.25
+#define ORC_INF_NU 2.5
 enum { ORC_TERM_ABSORBED = 0, ORC_TERM_LEAKED = 1, ORC_TERM_LOST = 2 };
 enum { ORC_N_SCORES = 4 }; /* flux, absorption, fission, nu-fission */
 enum { ORC_MAX_BATCHES = 512 };
@@ -101,6 +109,12 @@ int orc_hash_copy(const orc_problem* p, int nuc, int32_t* out);
 int orc_hash_bin(const orc_problem* p, double E);
 int orc_micro_xs(const orc_problem* p, int nuc, double E, int32_t* idx, double xs[4]);
 int orc_macro_xs(const orc_problem* p, int mat, double E, double xs[4]);
+/* macro_xs + the folded total after each 16-nuclide segment but the last
+ * (<= 16 values, count in *nck): what calculate_xs checkpoints for collision */
+int orc_macro_xs_ckpt(const orc_problem* p, int mat, double E, double xs[4], double* ck, int* nck);
+/* the same for n pairs: xs[4n], ck[16n], nck[n] */
+int orc_macro_xs_ckpt_n(const orc_problem* p, int64_t n, const int32_t* mat, const double* E, double* xs,
+                        double* ck, int32_t* nck);
 
 /* ---- deterministic math + RNG (golden vectors) ---- */
 double orc_log(double x);

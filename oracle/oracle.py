@@ -15,7 +15,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "liboracle.so")
 CLI_PATH = os.path.join(HERE, "_build", "openmc-oracle")
 
-PINCELL, ASSEMBLY, CORE = 0, 1, 2
+PINCELL, ASSEMBLY, CORE, INFINITE = 0, 1, 2, 3
+# the analytic infinite medium (omc_oracle.h ORC_INF_*)
+INF_SIGMA_T, INF_SIGMA_A, INF_SIGMA_F, INF_NU = 1.0, 0.4, 0.25, 2.5
 MAX_BATCHES = 512
 
 
@@ -82,6 +84,10 @@ def lib() -> C.CDLL:
         L.orc_hash_bin.argtypes = [P, C.c_double]
         L.orc_micro_xs.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_int32), C.c_double * 4]
         L.orc_macro_xs.argtypes = [P, C.c_int, C.c_double, C.c_double * 4]
+        L.orc_macro_xs_ckpt.argtypes = [P, C.c_int, C.c_double, C.c_double * 4, C.c_double * 16,
+                                        C.POINTER(C.c_int)]
+        L.orc_macro_xs_ckpt_n.argtypes = [P, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]
         L.orc_log.argtypes = [C.c_double]
         L.orc_log.restype = C.c_double
         L.orc_exp.argtypes = [C.c_double]
@@ -140,6 +146,29 @@ class Problem:
         if lib().orc_macro_xs(self._p, mat, E, out) != 0:
             raise RuntimeError(lib().orc_last_error().decode())
         return list(out)
+
+    def macro_ckpt(self, mat: int, E: float):
+        """(macro XS[4], segment checkpoints[:nck]) as calculate_xs stores them."""
+        out = (C.c_double * 4)()
+        ck = (C.c_double * 16)()
+        nck = C.c_int()
+        if lib().orc_macro_xs_ckpt(self._p, mat, E, out, ck, C.byref(nck)) != 0:
+            raise RuntimeError(lib().orc_last_error().decode())
+        return list(out), list(ck)[: nck.value]
+
+    def macro_ckpt_n(self, mat, E):
+        """Vectorised macro_ckpt: (xs [n, 4], ck [n, 16] (NaN past nck), nck [n])."""
+        import numpy as np
+        mat = np.ascontiguousarray(mat, np.int32)
+        E = np.ascontiguousarray(E, np.float64)
+        n = len(E)
+        xs = np.empty((n, 4), np.float64)
+        ck = np.full((n, 16), np.nan)
+        nck = np.empty(n, np.int32)
+        if lib().orc_macro_xs_ckpt_n(self._p, n, mat.ctypes.data, E.ctypes.data, xs.ctypes.data, ck.ctypes.data,
+                                     nck.ctypes.data) != 0:
+            raise RuntimeError(lib().orc_last_error().decode())
+        return xs, ck, nck
 
     def grid(self, nuc: int):
         import numpy as np

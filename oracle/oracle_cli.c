@@ -38,6 +38,7 @@ int main(int argc, char** argv) {
     int kind = ORC_ASSEMBLY;
     if (prob && !strcmp(prob, "pincell")) kind = ORC_PINCELL;
     else if (prob && !strcmp(prob, "core")) kind = ORC_CORE;
+    else if (prob && !strcmp(prob, "infinite")) kind = ORC_INFINITE;
     orc_problem* p = NULL;
     if (orc_problem_create(kind, (uint64_t)env_long("OMCG_XS_SEED", 1234), (int)bins, &p) != 0) {
         fprintf(stderr, "openmc-oracle: %s\n", orc_last_error());

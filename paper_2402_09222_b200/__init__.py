@@ -18,18 +18,19 @@ Python names mirror the reference's interfaces for this path:
 from __future__ import annotations
 
 import ctypes as C
+import math
 import time
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _omcg
-from ._omcg import (ASSEMBLY, BIND_CORES, BIND_SOCKETS, BIND_THREADS, CORE, N_SCORES, PINCELL,
+from ._omcg import (ASSEMBLY, BIND_CORES, BIND_SOCKETS, BIND_THREADS, CORE, INFINITE, N_SCORES, PINCELL,
                     QUEUED, QUEUELESS, Record, RunConfig, RunResult)
 
 _lib = _omcg.load()  # raises ImportError if the CUDA extension is missing
 
-KINDS = {"pincell": PINCELL, "assembly": ASSEMBLY, "core": CORE}
+KINDS = {"pincell": PINCELL, "assembly": ASSEMBLY, "core": CORE, "infinite": INFINITE}
 RECORD_DTYPE = np.dtype([("n_xs", "<i4"), ("n_adv", "<i4"), ("n_cross", "<i4"), ("n_coll", "<i4"),
                          ("n_sites", "<i4"), ("term", "<i4"), ("e_final", "<f8"), ("x_final", "<f8")])
 
@@ -95,6 +96,18 @@ class Problem:
                                    out.ctypes.data))
         return out
 
+    def xs_lookup_queue(self, n_bins: int, mat, E, sort_threshold: int | None = None, device: int = 0):
+        """The production fuel calculate_xs kernel on a queue (sorted when
+        len >= sort_threshold): (macro XS [n, 4], segment checkpoints [n, 16])."""
+        mat = np.ascontiguousarray(mat, np.int32)
+        E = np.ascontiguousarray(E, np.float64)
+        out = np.empty((len(E), 4), np.float64)
+        ck = np.empty((len(E), 16), np.float64)
+        _check(_lib.omcg_xs_lookup_queue(self._p, n_bins, device, len(E), mat.ctypes.data, E.ctypes.data,
+                                         -1 if sort_threshold is None else int(sort_threshold),
+                                         out.ctypes.data, ck.ctypes.data))
+        return out, ck
+
 
 @dataclass
 class RunOutput:
@@ -108,7 +121,8 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
                 host_threads=8, tasks_per_gpu=1, cpu_bind="threads", n_particles=1_000_000,
                 n_batches=15, n_inactive=5, seed=1, n_gpus=1, devices=None, world_size=1, rank=0,
                 nccl_id: bytes | None = None, record_batch=0, record_n=0, profile=False,
-                trace_queues=False, tail_threshold=None, event_fusion=None, move_event_cap=None) -> RunConfig:
+                trace_queues=False, tail_threshold=None, event_fusion=None, move_event_cap=None,
+                force_nccl=False) -> RunConfig:
     cfg = RunConfig()
     _lib.omcg_run_config_default(C.byref(cfg))
     m = {"openmc": QUEUED, "queued": QUEUED, "openmc-queueless": QUEUELESS,
@@ -144,6 +158,7 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
         cfg.event_fusion = int(event_fusion)
     if move_event_cap is not None:
         cfg.move_event_cap = int(move_event_cap)
+    cfg.force_nccl = int(bool(force_nccl))
     return cfg
 
 
@@ -192,7 +207,10 @@ def evaluate(config: dict, problem: Problem | None = None, penalty: float = -1.0
                   n_bins=int(config.get("P2", 4000)), sort_threshold=sort,
                   host_threads=int(config.get("P4", 8)), tasks_per_gpu=int(config.get("P5", 1)),
                   cpu_bind=config.get("P6", "threads"), **run_kw)
-        return {"objective": out.result.fom, "status": "ok", "elapsed": time.perf_counter() - t0,
-                "energy_j": out.result.energy_j}
-    except Exception:  # noqa: BLE001 — the contract turns every failure into 'fail'
-        return {"objective": penalty, "status": "fail", "elapsed": time.perf_counter() - t0}
+        fom = float(out.result.fom)
+        if not math.isfinite(fom) or fom <= 0.0:  # a non-finite objective is a failure (ensemble.cpp:188-191)
+            raise RuntimeError(f"non-finite or empty FoM {fom}")
+        return {"objective": fom, "status": "ok", "elapsed": time.perf_counter() - t0,
+                "energy_j": out.result.energy_j, "k_eff": out.result.k_mean}
+    except Exception as e:  # noqa: BLE001 — the contract turns every failure into 'fail'
+        return {"objective": penalty, "status": "fail", "elapsed": time.perf_counter() - t0, "message": str(e)}

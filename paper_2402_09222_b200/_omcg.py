@@ -11,14 +11,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libomcg.so")
-# A/B of compile-time variants on one GPU box: another build of this library
-# (a file named libomcg*.so) may be selected with OMCG_LIB_AB
-_ab = os.environ.get("OMCG_LIB_AB")
-if _ab and os.path.basename(_ab).startswith("libomcg") and _ab.endswith(".so"):
-    LIB_PATH = _ab
 
 OMCG_OK, OMCG_EINVAL, OMCG_EIO, OMCG_ECUDA, OMCG_ENCCL, OMCG_EFAIL = range(6)
-PINCELL, ASSEMBLY, CORE = 0, 1, 2
+PINCELL, ASSEMBLY, CORE, INFINITE = 0, 1, 2, 3
 QUEUED, QUEUELESS = 0, 1
 BIND_CORES, BIND_THREADS, BIND_SOCKETS = 0, 1, 2
 N_SCORES = 4
@@ -28,6 +23,7 @@ MAX_BATCHES = 512
 EXPORTS = (
     "omcg_version", "omcg_last_error", "omcg_problem_create", "omcg_problem_free",
     "omcg_problem_get_info", "omcg_library_checksum", "omcg_hash_build", "omcg_xs_lookup",
+    "omcg_xs_lookup_queue",
     "omcg_run_config_default", "omcg_run", "omcg_queue_trace", "omcg_nccl_unique_id",
     "omcg_device_count", "omcg_bank_exchange_plan",
 )
@@ -50,7 +46,7 @@ class RunConfig(C.Structure):
         ("devices", C.c_int * 8), ("world_size", C.c_int), ("rank", C.c_int),
         ("nccl_id", C.c_ubyte * 128), ("record_batch", C.c_int), ("record_n", C.c_int64),
         ("profile", C.c_int), ("trace_queues", C.c_int), ("tail_threshold", C.c_int64),
-        ("event_fusion", C.c_int), ("move_event_cap", C.c_int),
+        ("event_fusion", C.c_int), ("move_event_cap", C.c_int), ("force_nccl", C.c_int),
     ]
 
 
@@ -94,6 +90,8 @@ def load() -> C.CDLL:
     lib.omcg_library_checksum.restype = C.c_uint64
     lib.omcg_hash_build.argtypes = [P, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.c_void_p]
     lib.omcg_xs_lookup.argtypes = [P, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.omcg_xs_lookup_queue.argtypes = [P, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                         C.c_void_p, C.c_void_p]
     lib.omcg_run_config_default.argtypes = [C.POINTER(RunConfig)]
     lib.omcg_run_config_default.restype = None
     lib.omcg_run.argtypes = [P, C.POINTER(RunConfig), C.POINTER(RunResult), C.c_void_p, C.c_void_p]

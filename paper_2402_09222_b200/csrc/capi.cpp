@@ -109,6 +109,16 @@ OMCG_API int omcg_xs_lookup(const omcg_problem* p, int n_bins, int device, int64
     });
 }
 
+OMCG_API int omcg_xs_lookup_queue(const omcg_problem* p, int n_bins, int device, int64_t n, const int32_t* mat,
+                                  const double* E, int64_t sort_threshold, double* out, double* ckpt_out) {
+    return wrap([&] {
+        if (!p || (n > 0 && (!mat || !E || !out))) throw std::invalid_argument("null argument");
+        if (n < 0) throw std::invalid_argument("n < 0");
+        if (n_bins < 1 || n_bins > 1000000) throw std::invalid_argument("n_bins out of range [1, 1e6]");
+        if (n == 0) return;
+        omcg::device_xs_lookup_queue(p->p, n_bins, device, n, mat, E, sort_threshold, out, ckpt_out);
+    });
+}
 OMCG_API void omcg_run_config_default(omcg_run_config* c) {
     if (!c) return;
     std::memset(c, 0, sizeof *c);

@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "device.cuh"
 
 namespace omcg {
@@ -45,8 +47,15 @@ struct Ctx {
 
 constexpr int SMEM_TALLY_MAX = 64;  // tally bins*scores aggregated per block in smem (few-pin problems)
 
-// bookkeeping
-void reset_launch_counter();
+// bookkeeping: kernel launches are counted into the counter installed on the
+// calling host thread (one per omcg_run), else into a process-wide counter
+struct LaunchCounterScope {
+    explicit LaunchCounterScope(std::atomic<long long>* c);
+    ~LaunchCounterScope();
+    LaunchCounterScope(const LaunchCounterScope&) = delete;
+    LaunchCounterScope& operator=(const LaunchCounterScope&) = delete;
+    std::atomic<long long>* prev;
+};
 long long launch_counter();
 
 // library / hash
@@ -54,14 +63,17 @@ void launch_hash_build(const DevLib& lib, int32_t* hash, cudaStream_t s);
 void launch_xs_pairs(const DevLib& lib, int64_t n, const int32_t* mat, const double* E, double* out,
                      cudaStream_t s);
 
+// parity hook: slots 0..n-1 wait for calculate_xs at (mat[i], E[i]); q[i] = i
+void launch_lookup_setup(const Ctx& c, int n, const int32_t* mat, const double* E, int32_t* q, cudaStream_t s);
+
 // event kernels; q == nullptr selects the queueless variant over all cap slots
 void launch_init(const Ctx& c, uint64_t head, int n, int64_t first_local, const Site* src, cudaStream_t s);
-// list != nullptr: warp-per-history tail over the `live` remaining histories
-// (ctrl[3] must be zero); nullptr: thread-per-slot tail
+// warp-per-history tail over the `live` remaining histories, listed into
+// `list` first (ctrl[3] must be zero)
 void launch_tail(const Ctx& c, bool queued, int64_t live, int32_t* list, cudaStream_t s);
 void launch_refill_all(const Ctx& c, int64_t first_local, int64_t n_remaining, const Site* src,
                        cudaStream_t s);
-void launch_xs(const Ctx& c, const int32_t* q, int n, bool fuel, cudaStream_t s);
+void launch_xs(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 // fuel-queue calculate_xs split by 16-nuclide segment in one launch: a block
 // per 32 entries, segment partials in shared memory, in-order fold by warp 0
 // (nseg <= 48); same arithmetic as launch_xs
@@ -75,9 +87,9 @@ void launch_collide(const Ctx& c, const int32_t* q, int n, int n_front, cudaStre
 // fused transport: every history of the move queue runs advance / crossing /
 // non-fuel calculate_xs / non-fuel collision in registers until it needs a
 // fuel lookup, collides in fuel or dies
-// coll_in: non-fuel collisions run inside the loop (always for the queueless
-// sweep; for the queued end of a batch it measured neutral, so it is unused there)
-void launch_move(const Ctx& c, const int32_t* q, int n, cudaStream_t s, bool coll_in = false);
+// (the queueless sweep, q == nullptr, runs the non-fuel collisions inside the
+// loop too)
+void launch_move(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 // diagnostic build only (-DOMCG_MOVE_CYCLES): per-event-type cycle shares of k_move to stderr
 void dump_move_cycles();
 

@@ -19,6 +19,7 @@ struct NcclApi {
     decltype(&ncclCommInitRank) CommInitRank = nullptr;
     decltype(&ncclCommInitAll) CommInitAll = nullptr;
     decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclCommAbort) CommAbort = nullptr;
     decltype(&ncclAllReduce) AllReduce = nullptr;
     decltype(&ncclAllGather) AllGather = nullptr;
     decltype(&ncclSend) Send = nullptr;
@@ -46,6 +47,7 @@ inline NcclApi& nccl() {
         OMCG_NCCL_SYM(CommInitRank, ncclCommInitRank)
         OMCG_NCCL_SYM(CommInitAll, ncclCommInitAll)
         OMCG_NCCL_SYM(CommDestroy, ncclCommDestroy)
+        OMCG_NCCL_SYM(CommAbort, ncclCommAbort)
         OMCG_NCCL_SYM(AllReduce, ncclAllReduce)
         OMCG_NCCL_SYM(AllGather, ncclAllGather)
         OMCG_NCCL_SYM(Send, ncclSend)

@@ -127,6 +127,7 @@ int main(int argc, char** argv) {
     int kind = OMCG_ASSEMBLY;
     if (prob && !std::strcmp(prob, "pincell")) kind = OMCG_PINCELL;
     else if (prob && !std::strcmp(prob, "core")) kind = OMCG_CORE;
+    else if (prob && !std::strcmp(prob, "infinite")) kind = OMCG_INFINITE;
     cfg.n_particles = env_ll("OMCG_PARTICLES", cfg.n_particles);
     cfg.n_batches = (int)env_ll("OMCG_BATCHES", cfg.n_batches);
     cfg.n_inactive = (int)env_ll("OMCG_INACTIVE", cfg.n_inactive);

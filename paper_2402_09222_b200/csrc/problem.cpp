@@ -189,12 +189,54 @@ uint64_t library_checksum(const Problem& p) {
     return h;
 }
 
+// Analytic check problem (kind INFINITE): an infinite homogeneous medium of
+// one nuclide whose cross sections do not depend on energy (reflective box,
+// every region the same material). Its expectations are exact and
+// independent of this code base: k_inf = nu*Sigma_f / Sigma_a, every history
+// is absorbed (the absorption estimator scores k_inf exactly), the mean number
+// of collisions per history is Sigma_t / Sigma_a and the mean track length per
+// history 1 / Sigma_a.
+void build_infinite(Problem& p) {
+    const double ln_range = det_log(E_MAX) - det_log(E_MIN);
+    const int ng = INF_GRID;
+    p.n_nuc = 1;
+    p.global_id.assign(1, -1);
+    p.awr.assign(1, INF_AWR);
+    p.goff = {0, ng};
+    p.E.resize(ng);
+    p.xs.assign(ng, XS4{INF_SIGMA_T, INF_SIGMA_A, INF_SIGMA_F, INF_NU * INF_SIGMA_F});
+    for (int i = 0; i < ng; ++i) p.E[i] = E_MIN * det_exp((double)i / (double)(ng - 1) * ln_range);
+    p.E[0] = E_MIN;
+    p.E[ng - 1] = E_MAX;
+    p.mat.resize(3);
+    for (auto& m : p.mat) {
+        m.nuc = {0};
+        m.dens = {1.0};
+        m.fissionable = true;
+    }
+    Geometry& G = p.geo;
+    for (auto& t : G.pt) t = PinType{0, {0.0, 0.0}, {MAT_FUEL, MAT_FUEL, MAT_FUEL}};
+    G.pitch = 1.26;
+    G.nx = G.ny = 1;
+    G.bc_x = G.bc_y = G.bc_z = 1;
+    G.x0 = G.y0 = -0.63;
+    G.z_lo = -100.0;
+    G.z_hi = 100.0;
+    p.pin_map_host.assign(1, 0);
+    G.pin_map = p.pin_map_host.data();
+}
+
 void build_problem(Problem& p, int kind, uint64_t xs_seed, int n_threads) {
-    if (kind < PINCELL || kind > CORE) throw std::invalid_argument("unknown problem kind");
+    if (kind < PINCELL || kind > INFINITE) throw std::invalid_argument("unknown problem kind");
     auto t0 = std::chrono::steady_clock::now();
     p = Problem();
     p.kind = kind;
     p.xs_seed = xs_seed;
+    if (kind == INFINITE) {
+        build_infinite(p);
+        p.gen_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return;
+    }
 
     // material compositions in global ids (largest contributors first)
     std::vector<int> mg[3];

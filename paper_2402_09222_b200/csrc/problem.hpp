@@ -17,7 +17,11 @@
 
 namespace omcg {
 
-enum ProblemKind { PINCELL = 0, ASSEMBLY = 1, CORE = 2 };
+enum ProblemKind { PINCELL = 0, ASSEMBLY = 1, CORE = 2, INFINITE = 3 };
+// the analytic infinite-medium problem (one energy-independent nuclide, density 1 atom/(b cm))
+constexpr int INF_GRID = 1001;
+constexpr double INF_AWR = 12.0;
+constexpr double INF_SIGMA_T = 1.0, INF_SIGMA_A = 0.4, INF_SIGMA_F = 0.25, INF_NU = 2.5;
 enum MaterialId { MAT_WATER = 0, MAT_CLAD = 1, MAT_FUEL = 2 };
 
 struct alignas(32) XS4 {

@@ -37,6 +37,7 @@ inline NcclApi& nccl_checked() {
 #define ncclCommInitRank omcg::nccl_checked().CommInitRank
 #define ncclCommInitAll omcg::nccl_checked().CommInitAll
 #define ncclCommDestroy omcg::nccl_checked().CommDestroy
+#define ncclCommAbort omcg::nccl_checked().CommAbort
 #define ncclAllReduce omcg::nccl_checked().AllReduce
 #define ncclAllGather omcg::nccl_checked().AllGather
 #define ncclSend omcg::nccl_checked().Send
@@ -64,8 +65,8 @@ using ull = unsigned long long;
 
 namespace {
 
-std::mutex g_trace_mu;
-std::vector<int64_t> g_trace;
+// queue trace of the calling thread's last omcg_run (trace_queues != 0)
+thread_local std::vector<int64_t> t_trace;
 
 // Device allocations owned by one object, freed on destruction. They come
 // from the device's stream-ordered memory pool with the release threshold
@@ -145,36 +146,6 @@ struct GpuProblem {
     int n_fuel_mats = 0;
     int max_fuel_seg = 1;  // 16-nuclide segments of the largest fuel-queue material
     int64_t h2d_bytes = 0;
-    void* lib_base = nullptr;  // rows, then energies, then the hash grid: contiguous
-    size_t lib_bytes = 0;
-    void* search_base = nullptr;  // energies + hash grid (what the bracket search reads)
-    size_t search_bytes = 0;
-
-    // Opt-in (OMCG_L2_PERSIST=1: the whole library, =2: only the energy grids
-    // and hash grid the bracket search reads): ask L2 to keep it resident
-    // against the streaming particle records (cudaAccessPolicyWindow on the
-    // stream). Measured on B200 (C2): whole library 8.26M -> 6.03M FoM, search
-    // data only 15.1M -> 14.3M, so it is off by default.
-    void l2_persist(cudaStream_t s, int device) const {
-        const char* v = std::getenv("OMCG_L2_PERSIST");
-        if (!v || std::atoi(v) == 0) return;
-        const bool search_only = std::atoi(v) == 2;
-        int max_persist = 0, max_window = 0;
-        if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device) != cudaSuccess ||
-            cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device) != cudaSuccess ||
-            max_persist <= 0 || max_window <= 0)
-            return;
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
-        cudaStreamAttrValue attr{};
-        attr.accessPolicyWindow.base_ptr = search_only ? search_base : lib_base;
-        attr.accessPolicyWindow.num_bytes = std::min(search_only ? search_bytes : lib_bytes, (size_t)max_window);
-        attr.accessPolicyWindow.hitRatio =
-            std::min(1.0f, (float)max_persist / (float)attr.accessPolicyWindow.num_bytes);
-        attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &attr);
-        cudaGetLastError();  // best effort
-    }
 
     void upload(const Problem& p, int n_bins, int device, cudaStream_t s) {
         arena.device = device;
@@ -226,18 +197,13 @@ struct GpuProblem {
             h2d_bytes += (int64_t)bytes;
         };
         int32_t* d_goff = arena.alloc<int32_t>(nn + 1);
-        // grid energies and rows in one allocation so one L2 access-policy
-        // window can cover the whole library
+        // rows, then grid energies, then the hash grid: one allocation
         const int64_t npts = p.grid_points();
         const int64_t hash_n = (int64_t)(n_bins + 1) * nn;
         char* d_lib = arena.alloc<char>(npts * (int64_t)(sizeof(double) + sizeof(XS4)) +
                                         hash_n * (int64_t)sizeof(int32_t) + 256);
         XS4* d_xs = reinterpret_cast<XS4*>(d_lib);
         double* d_E = reinterpret_cast<double*>(d_lib + npts * (int64_t)sizeof(XS4));
-        lib_base = d_lib;
-        lib_bytes = (size_t)npts * (sizeof(double) + sizeof(XS4)) + sizeof(int32_t) * (size_t)hash_n;
-        search_base = d_E;
-        search_bytes = (size_t)npts * sizeof(double) + sizeof(int32_t) * (size_t)hash_n;
         double* d_awr = arena.alloc<double>(nn);
         int32_t* d_moff = arena.alloc<int32_t>(nm + 1);
         int32_t* d_mnuc = arena.alloc<int32_t>((int64_t)mnuc.size());
@@ -318,6 +284,7 @@ struct Rank {
     int device = 0, rank = 0, world = 1;
     ncclComm_t comm = nullptr;
     BatchComm* bc = nullptr;          // per-batch collectives (NCCL or in-process loopback)
+    std::atomic<long long>* launches = nullptr;  // the call's kernel-launch counter
     std::vector<ull> sall;            // bank sizes of all ranks, this batch
     DevArena arena;
     GpuProblem gp;
@@ -349,8 +316,6 @@ struct Rank {
     std::string error;
 };
 
-int xs_fuel_mode();
-
 // ------------------------------------------------------------------ setup
 void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     auto t0 = std::chrono::steady_clock::now();
@@ -381,7 +346,7 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, R.device);
         const int64_t per = 4 * (int64_t)R.n_tally_bins * (int64_t)sizeof(ull);
-        R.n_priv = 4 * R.n_tally_bins <= SMEM_TALLY_MAX || !env_flag("OMCG_TALLY_PRIV")
+        R.n_priv = 4 * R.n_tally_bins <= SMEM_TALLY_MAX
                        ? 0
                        : (int)std::max<int64_t>(1, std::min<int64_t>(sms, (64LL << 20) / per));
         if (R.n_priv > 0) {
@@ -399,7 +364,7 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     if (cfg.record_batch > 0 && cfg.record_n > 0) R.acc.records = R.arena.alloc<omcg_record>(cfg.record_n);
     R.source = R.arena.alloc<Site>(R.N_rank);
     R.canon = R.arena.alloc<Site>(R.bank_cap);
-    if (R.world > 1) R.recv = R.arena.alloc<Site>(R.bank_cap + R.N_rank);
+    if (R.bc) R.recv = R.arena.alloc<Site>(R.bank_cap + R.N_rank);
     R.scan_out = R.arena.alloc<int64_t>(R.N_rank);
     R.scan_tmp = R.arena.alloc<int64_t>((R.N_rank + 1023) / 1024 + 1);
     R.d_sall = R.arena.alloc<ull>(R.world);
@@ -421,7 +386,6 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         S.b.cap = cap;
         S.prof_level = cfg.profile;
         CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
-        R.gp.l2_persist(S.stream, R.device);
         Bank& B = S.b;
         B.p = A.alloc<PState>(cap);
         B.cnt = A.alloc<int4>(cap);
@@ -499,21 +463,9 @@ void teardown_rank(Rank& R) {
 }
 
 // ------------------------------------------------------------------ event loops
-// A/B switches: OMCG_XS_SPLIT=0 selects the one-history-per-thread fuel
-// lookup, OMCG_TAIL_WARP=0 the thread-per-history tail.
-bool env_flag(const char* name) {
+bool env_flag(const char* name) {  // unset or nonzero -> true
     const char* v = std::getenv(name);
     return !v || std::atoi(v) != 0;
-}
-// fuel calculate_xs variant: 2 split by segment in one launch (default), 0 one
-// history per thread (OMCG_XS_SPLIT=0)
-int xs_fuel_mode() {
-    static const int m = !env_flag("OMCG_XS_SPLIT") ? 0 : 2;
-    return m;
-}
-bool tail_warp() {
-    static const bool on = env_flag("OMCG_TAIL_WARP");
-    return on;
 }
 
 // Per-kernel CUDA-event timing on the launching stream. Events are recorded
@@ -565,7 +517,6 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
     // next queue lengths exactly and skips the read-back and its sync.
     bool known = false, check_prediction = false;
     unsigned predicted[8];
-    static const bool predict = env_flag("OMCG_PREDICT_COUNTS");
     for (;;) {
         if (!known) {
             CK(cudaMemcpyAsync(S.h_counts, S.qs.count, sizeof(unsigned) * 8, cudaMemcpyDeviceToHost, S.stream));
@@ -608,7 +559,7 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                 n = (int)live;
                 CK(cudaMemsetAsync(S.ctrl + 3, 0, sizeof(ull), S.stream));
                 Prof pf(S, prof, 7, live);
-                launch_tail(c, true, live, tail_warp() ? S.tail_list : nullptr, S.stream);
+                launch_tail(c, true, live, S.tail_list, S.stream);
                 S.tail_launches++;
             } else {
                 const int32_t* qptr = S.qs.qbase + (int64_t)(best == EV_ADV ? c.qs.adv_q : best) * S.qs.cap;
@@ -623,12 +574,10 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                     }
                     {
                         Prof pf(S, prof, 0, n);
-                        const int xm = xs_fuel_mode();
-                        if (xm == 2) launch_xs_fuel_fused(c, qptr, n, R.gp.max_fuel_seg, S.stream);
-                        else launch_xs(c, qptr, n, true, S.stream);
+                        launch_xs_fuel_fused(c, qptr, n, R.gp.max_fuel_seg, S.stream);
                     }
                     if (prof) S.xs_fuel_bytes += (double)n * (44.0 + 100.0 * (double)fuel_nuc);
-                    if (predict && c.fused && !(dead > 0 && next < S.hi)) {
+                    if (c.fused && !(dead > 0 && next < S.hi)) {
                         S.h_counts[EV_ADV] += (unsigned)n;  // the move queue receives every entry
                         S.h_counts[EV_XS_FUEL] = 0u;
                         if (trace) {  // trace mode reads back anyway and checks the prediction
@@ -639,7 +588,7 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
                         }
                     }
                     break;
-                case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, false, S.stream); } break;
+                case EV_XS_NONFUEL: { Prof pf(S, prof, 1, n); launch_xs(c, qptr, n, S.stream); } break;
                 case EV_ADV: {
                     Prof pf(S, prof, 2, n);
                     if (c.fused && c.move_cap)  // capped histories go to the other region
@@ -688,7 +637,7 @@ void run_queueless(Rank& R, SubBank& S, Ctx c, const Site* src, bool prof, int64
             { Prof pf(S, prof, 2, cap); launch_move(c, nullptr, cap, S.stream); }
             { Prof pf(S, prof, 4, cap); launch_collide(c, nullptr, 0, 0, S.stream); }
         } else {
-            { Prof pf(S, prof, 0, S.b.cap); launch_xs(c, nullptr, 0, false, S.stream); }
+            { Prof pf(S, prof, 0, S.b.cap); launch_xs(c, nullptr, 0, S.stream); }
             { Prof pf(S, prof, 2, S.b.cap); launch_advance(c, nullptr, 0, S.stream); }
             { Prof pf(S, prof, 3, S.b.cap); launch_cross(c, nullptr, 0, S.stream); }
             { Prof pf(S, prof, 4, S.b.cap); launch_collide(c, nullptr, 0, 0, S.stream); }
@@ -703,7 +652,7 @@ void run_queueless(Rank& R, SubBank& S, Ctx c, const Site* src, bool prof, int64
         if (next >= S.hi && alive <= tail) {
             CK(cudaMemsetAsync(S.ctrl + 3, 0, sizeof(ull), S.stream));
             Prof pf(S, prof, 7, alive);
-            launch_tail(c, false, alive, tail_warp() ? S.tail_list : nullptr, S.stream);
+            launch_tail(c, false, alive, S.tail_list, S.stream);
             S.tail_launches++;
             CK(cudaStreamSynchronize(S.stream));
             break;
@@ -772,20 +721,28 @@ struct LoopbackShared {
     std::condition_variable cv;
     int count = 0;
     uint64_t gen = 0;
+    bool aborted = false;  // a rank failed: every barrier throws instead of waiting for it
     std::vector<std::vector<ull>> host;
     std::vector<Site*> canon;
     std::vector<double> vals;
     explicit LoopbackShared(int w) : world(w), host(w), canon(w), vals(w) {}
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
+        if (aborted) throw std::runtime_error("another rank of this run failed");
         const uint64_t g = gen;
         if (++count == world) {
             count = 0;
             ++gen;
             cv.notify_all();
         } else {
-            cv.wait(lk, [&] { return gen != g; });
+            cv.wait(lk, [&] { return gen != g || aborted; });
+            if (gen == g) throw std::runtime_error("another rank of this run failed");
         }
+    }
+    void abort() {
+        std::lock_guard<std::mutex> lk(mu);
+        aborted = true;
+        cv.notify_all();
     }
 };
 
@@ -842,6 +799,121 @@ struct LoopbackBatchComm : BatchComm {
     }
 };
 
+// NCCL communicators cost tens to hundreds of ms to create, so they are kept
+// for the life of the process and reused by later omcg_run calls with the
+// same placement (an in-process evaluator or bench pass calls omcg_run many
+// times). A communicator is leased by one call at a time; a concurrent call
+// with the same placement gets its own. One that saw a failure is aborted and
+// dropped.
+struct CommCache {
+    struct Entry {
+        std::string key;
+        std::vector<ncclComm_t> comms;
+        bool busy = false;
+    };
+    std::mutex mu;
+    std::vector<std::unique_ptr<Entry>> entries;
+};
+CommCache& comm_cache() {
+    static CommCache* c = new CommCache();  // process lifetime
+    return *c;
+}
+
+struct CommLease {
+    CommCache::Entry* e = nullptr;
+    std::vector<ncclComm_t> comms;
+    std::atomic<bool> aborted{false};
+
+    CommCache::Entry* find_or_add(const std::string& key, bool& fresh) {
+        CommCache& C = comm_cache();
+        std::lock_guard<std::mutex> lk(C.mu);
+        for (auto& x : C.entries)
+            if (x->key == key && !x->busy) {
+                x->busy = true;
+                fresh = false;
+                return x.get();
+            }
+        C.entries.emplace_back(new CommCache::Entry());
+        CommCache::Entry* x = C.entries.back().get();
+        x->key = key;
+        x->busy = true;
+        fresh = true;
+        return x;
+    }
+    void drop_entry() {
+        CommCache& C = comm_cache();
+        std::lock_guard<std::mutex> lk(C.mu);
+        for (size_t i = 0; i < C.entries.size(); ++i)
+            if (C.entries[i].get() == e) {
+                C.entries.erase(C.entries.begin() + (long)i);
+                break;
+            }
+        e = nullptr;
+    }
+    // one rank of a multi-process job (ncclCommInitRank)
+    void acquire_rank(const unsigned char id_bytes[128], int world, int rank, int device) {
+        char hex[2 * 128 + 1];
+        for (int i = 0; i < 128; ++i) std::snprintf(hex + 2 * i, 3, "%02x", id_bytes[i]);
+        const std::string key = "rank " + std::to_string(world) + ":" + std::to_string(rank) + ":" +
+                                std::to_string(device) + ":" + hex;
+        bool fresh = false;
+        e = find_or_add(key, fresh);
+        if (fresh) {
+            try {
+                ncclUniqueId id;
+                std::memcpy(id.internal, id_bytes, 128);
+                ncclComm_t c = nullptr;
+                CK(cudaSetDevice(device));
+                NK(ncclCommInitRank(&c, world, id, rank));
+                e->comms.assign(1, c);
+            } catch (...) {
+                drop_entry();
+                throw;
+            }
+        }
+        comms = e->comms;
+    }
+    // every rank in this process, one GPU each (ncclCommInitAll; also a
+    // one-rank communicator when NCCL is forced on one GPU)
+    void acquire_all(const std::vector<int>& devs) {
+        std::string key = "all";
+        for (int d : devs) key += " " + std::to_string(d);
+        bool fresh = false;
+        e = find_or_add(key, fresh);
+        if (fresh) {
+            try {
+                std::vector<ncclComm_t> c(devs.size(), nullptr);
+                NK(ncclCommInitAll(c.data(), (int)devs.size(), devs.data()));
+                e->comms = c;
+            } catch (...) {
+                drop_entry();
+                throw;
+            }
+        }
+        comms = e->comms;
+    }
+    // called by a failing rank: unblocks the others' collectives
+    void abort() {
+        if (!e || aborted.exchange(true)) return;
+        for (ncclComm_t c : comms)
+            if (c) ncclCommAbort(c);
+    }
+    void release(bool failed) {
+        if (!e) return;
+        if (failed || aborted) {
+            if (!aborted)
+                for (ncclComm_t c : comms)
+                    if (c) ncclCommAbort(c);
+            drop_entry();
+            return;
+        }
+        std::lock_guard<std::mutex> lk(comm_cache().mu);
+        e->busy = false;
+        e = nullptr;
+    }
+    ~CommLease() { release(true); }  // only reached with e set if release() was skipped (exception)
+};
+
 // ------------------------------------------------------------------ batches
 void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     CK(cudaSetDevice(R.device));
@@ -883,8 +955,6 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         base.recording = (R.acc.records && batch == cfg.record_batch) ? 1 : 0;
         base.fused = cfg.event_fusion ? 1 : 0;
         base.move_cap = cfg.event_fusion ? std::max(0, cfg.move_event_cap) : 0;
-        if (cfg.event_fusion && std::getenv("OMCG_MOVE_CAP_AB"))  // A/B override (scripts/ab.sh)
-            base.move_cap = std::atoi(std::getenv("OMCG_MOVE_CAP_AB"));
         const Site* src = have_source ? R.source : nullptr;
         const bool prof = cfg.profile != 0 && active;
 
@@ -907,6 +977,7 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
             std::vector<std::exception_ptr> errs(R.subs.size());
             for (size_t t = 0; t < R.subs.size(); ++t)
                 th.emplace_back([&, t] {
+                    LaunchCounterScope count_task(R.launches);
                     try { drive(R.subs[t]); } catch (...) { errs[t] = std::current_exception(); }
                 });
             for (auto& x : th) x.join();
@@ -922,7 +993,7 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         if (active && R.n_priv > 0)
             launch_tally_fold(R.tally_priv, R.n_priv, 4 * (int64_t)R.n_tally_bins, R.acc.tally, R.main);
         // ---- batch reduction (NCCL across ranks: integer sums are exact)
-        if (R.world > 1) {
+        if (R.bc) {  // NCCL (or the loopback between ranks sharing a GPU)
             R.bc->reduce_batch(R, active);
         } else {
             R.sall.assign(1, 0);
@@ -963,7 +1034,7 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         uint64_t bs = stream_seed(cfg.seed, (uint64_t)batch, STREAM_BANK);
         uint64_t off = (uint64_t)(prn(bs) * (double)S_total);
         if (off >= S_total) off = S_total - 1;
-        if (R.world == 1) {
+        if (!R.bc) {
             launch_resample(R.canon, 0, S_total, off, R.N, R.rank_lo, R.N_rank, R.source, R.main);
         } else {
             // each rank needs a contiguous slice of the global canonical bank
@@ -984,7 +1055,7 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, R.ev_a0, R.ev_a1));
     R.t_active = (double)ms * 1e-3;
-    if (R.world > 1) R.t_active = R.bc->max_over_ranks(R, R.t_active);  // max over ranks
+    if (R.bc) R.t_active = R.bc->max_over_ranks(R, R.t_active);  // max over ranks
 }
 
 void validate(const omcg_run_config& cfg) {
@@ -999,6 +1070,7 @@ void validate(const omcg_run_config& cfg) {
         throw std::invalid_argument("inactive batches must be in [0, batches)");
     if (cfg.world_size > 1 && (cfg.rank < 0 || cfg.rank >= cfg.world_size)) throw std::invalid_argument("bad rank");
     if (cfg.world_size > 1 && cfg.n_gpus > 1) throw std::invalid_argument("multi-process ranks use one GPU each");
+    if (cfg.force_nccl < 0 || cfg.force_nccl > 1) throw std::invalid_argument("force_nccl must be 0 or 1");
     if (cfg.n_gpus < 1 || cfg.n_gpus > 8) throw std::invalid_argument("n_gpus must be 1..8");
 }
 
@@ -1039,7 +1111,7 @@ void bank_exchange_plan(const uint64_t* S_all, int W, int64_t N, uint64_t off, i
     plan[4 * W + 1] = (int64_t)(my_b - my_a);
 }
 
-std::vector<int64_t>& last_queue_trace() { return g_trace; }
+std::vector<int64_t>& last_queue_trace() { return t_trace; }
 
 void nccl_unique_id(unsigned char out[128]) {
     ncclUniqueId id;
@@ -1140,38 +1212,43 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
     EnergyMeter meter;
     meter.start(meter_devs);
     mark("energy meter started");
-    reset_launch_counter();
+    std::atomic<long long> launches{0};  // this call's kernel launches (all of its host threads)
+    LaunchCounterScope count_here(&launches);
     std::vector<Rank> ranks(local_ranks);
-    std::vector<ncclComm_t> comms(local_ranks, nullptr);
     std::unique_ptr<LoopbackShared> loop_shared;
     std::vector<std::unique_ptr<BatchComm>> bcs(local_ranks);
+    CommLease lease;  // NCCL communicators: created once per placement, reused by later calls
     if (multiproc) {
-        ncclUniqueId id;
-        std::memcpy(id.internal, cfg.nccl_id, 128);
-        CK(cudaSetDevice(devs[0]));
-        NK(ncclCommInitRank(&comms[0], cfg.world_size, id, cfg.rank));
+        lease.acquire_rank(cfg.nccl_id, cfg.world_size, cfg.rank, devs[0]);
         bcs[0].reset(new NcclBatchComm());
     } else if (local_ranks > 1 && shared_gpu) {
         loop_shared.reset(new LoopbackShared(local_ranks));
         for (int i = 0; i < local_ranks; ++i) bcs[i].reset(new LoopbackBatchComm(loop_shared.get()));
-    } else if (local_ranks > 1) {
-        NK(ncclCommInitAll(comms.data(), local_ranks, devs.data()));
+    } else if (local_ranks > 1 || cfg.force_nccl) {
+        lease.acquire_all(devs);
         for (int i = 0; i < local_ranks; ++i) bcs[i].reset(new NcclBatchComm());
     }
+    mark("communicators");
     for (int i = 0; i < local_ranks; ++i) {
         ranks[i].device = devs[i];
-        ranks[i].comm = comms[i];
+        ranks[i].comm = lease.comms.empty() ? nullptr : lease.comms[i];
         ranks[i].bc = bcs[i].get();
         ranks[i].world = multiproc ? cfg.world_size : local_ranks;
         ranks[i].rank = multiproc ? cfg.rank : i;
+        ranks[i].launches = &launches;
     }
     std::vector<std::exception_ptr> errs(local_ranks);
     auto body = [&](int i) {
+        LaunchCounterScope count_rank(&launches);
         try {
             setup_rank(ranks[i], p, cfg);
             run_rank(ranks[i], p, cfg);
         } catch (...) {
             errs[i] = std::current_exception();
+            // the other ranks of this call must not wait for this one forever:
+            // loopback barriers throw, NCCL collectives are aborted
+            if (loop_shared) loop_shared->abort();
+            if (local_ranks > 1) lease.abort();
         }
     };
     if (local_ranks == 1) body(0);
@@ -1230,7 +1307,7 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
         res->t_init = ti;
         res->fom = ta > 0.0 ? (double)cfg.n_particles * (double)n_active / ta : 0.0;
         res->kernel_launches = R0.launches_active;
-        res->kernel_launches_total = launch_counter();
+        res->kernel_launches_total = launches.load();
         if (tally_out) {
             std::memcpy(tally_out, R0.tally_total.data(), sizeof(int64_t) * R0.tally_total.size());
             res->d2h_bytes += 0;
@@ -1245,17 +1322,13 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
                                   cudaMemcpyDeviceToHost));
             }
         }
-        {
-            std::lock_guard<std::mutex> lk(g_trace_mu);
-            g_trace.clear();
-            for (auto& S : R0.subs) g_trace.insert(g_trace.end(), S.trace.begin(), S.trace.end());
-        }
+        t_trace.clear();
+        for (auto& S : R0.subs) t_trace.insert(t_trace.end(), S.trace.begin(), S.trace.end());
     }
     mark("results gathered");
     for (auto& R : ranks) teardown_rank(R);
     mark("streams/events destroyed");
-    for (auto c : comms)
-        if (c) ncclCommDestroy(c);
+    lease.release(first != nullptr);
     ranks.clear();  // device memory back before the call returns
     mark("teardown");
     res->energy_j = meter.stop_joules();
@@ -1305,6 +1378,99 @@ void device_xs_lookup(const Problem& p, int n_bins, int device, int64_t n, const
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(out, dout, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+    }
+    cudaStreamDestroy(s);
+}
+
+// The production fuel lookup on a queue: n histories waiting for
+// calculate_xs at (mat[i], E[i]) in the fuel XS queue (entry i = slot i),
+// sorted by (material, energy) when n >= sort_threshold >= 0 exactly as the
+// queued loop sorts it, then one k_xs_fuel_fused launch. out: the four
+// macroscopic XS per entry as stored in the record; ckpt_out (optional, n x 16):
+// the segment checkpoints (entries past the material's count untouched, NaN).
+// The launch must hand every entry on to the move queue: checked here.
+void device_xs_lookup_queue(const Problem& p, int n_bins, int device, int64_t n, const int32_t* mat, const double* E,
+                            int64_t sort_threshold, double* out, double* ckpt_out) {
+    if (n > (int64_t)1 << 30) throw std::invalid_argument("n too large");
+    for (int64_t i = 0; i < n; ++i)
+        if (mat[i] < 0 || mat[i] >= (int)p.mat.size()) throw std::invalid_argument("material out of range");
+    CK(cudaSetDevice(device));
+    cudaStream_t s;
+    CK(cudaStreamCreate(&s));
+    try {
+        GpuProblem gp;
+        gp.upload(p, n_bins, device, s);
+        int nseg = 1, n_sort_mats = 1;
+        for (const auto& m : p.mat) {
+            nseg = std::max(nseg, (int)((m.nuc.size() + CKPT_STRIDE - 1) / CKPT_STRIDE));
+            n_sort_mats += m.fissionable ? 1 : 0;
+        }
+        DevArena a;
+        a.device = device;
+        Ctx c{};
+        c.lib = gp.lib;
+        c.geo = gp.geo;
+        c.b.cap = n;
+        c.b.p = a.alloc<PState>(n);
+        c.b.xc = a.alloc<XsCache>(n);
+        c.b.cnt = a.alloc<int4>(n);
+        c.b.event = a.alloc<int8_t>(n);
+        c.b.ckpt = a.alloc<double>(NCKPT * n);
+        c.qs.cap = n;
+        c.qs.qbase = a.alloc<int32_t>((int64_t)(N_QUEUES + 1) * n);
+        c.qs.count = a.alloc<unsigned>(8);
+        c.qs.dead_tail = reinterpret_cast<ull*>(c.qs.count + 6);
+        c.qs.adv_q = EV_ADV;
+        c.ctrl = a.alloc<ull>(8);
+        int32_t* sorted = a.alloc<int32_t>(n);
+        uint32_t* keys = a.alloc<uint32_t>(n);
+        unsigned* hist = a.alloc<unsigned>((int64_t)n_sort_mats * 65536);
+        unsigned* cursor = a.alloc<unsigned>((int64_t)n_sort_mats * 65536);
+        unsigned* bsum = a.alloc<unsigned>((int64_t)n_sort_mats * 64);
+        int32_t* dm = a.alloc<int32_t>(n);
+        double* dE = a.alloc<double>(n);
+        CK(cudaMemsetAsync(c.qs.count, 0, sizeof(unsigned) * 8, s));
+        CK(cudaMemsetAsync(c.ctrl, 0, sizeof(ull) * 8, s));
+        CK(cudaMemsetAsync(hist, 0, sizeof(unsigned) * (size_t)n_sort_mats * 65536, s));
+        CK(cudaMemsetAsync(c.b.ckpt, 0xff, sizeof(double) * NCKPT * (size_t)n, s));
+        CK(cudaMemcpyAsync(dm, mat, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dE, E, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        int32_t* q = c.qs.qbase + (int64_t)EV_XS_FUEL * n;
+        launch_lookup_setup(c, (int)n, dm, dE, q, s);
+        const int32_t* qptr = q;
+        if (sort_threshold >= 0 && n >= sort_threshold) {
+            launch_sort(c, q, sorted, (int)n, n_sort_mats, hist, cursor, keys, bsum, s);
+            qptr = sorted;
+        }
+        launch_xs_fuel_fused(c, qptr, (int)n, nseg, s);
+        CK(cudaGetLastError());
+        std::vector<PState> rec((size_t)n);
+        std::vector<int32_t> moved((size_t)n);
+        unsigned cnt[8];
+        CK(cudaMemcpyAsync(rec.data(), c.b.p, sizeof(PState) * (size_t)n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(moved.data(), c.qs.qbase + (int64_t)EV_ADV * n, sizeof(int32_t) * (size_t)n,
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(cnt, c.qs.count, sizeof cnt, cudaMemcpyDeviceToHost, s));
+        if (ckpt_out)
+            CK(cudaMemcpyAsync(ckpt_out, c.b.ckpt, sizeof(double) * NCKPT * (size_t)n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        // the launch appends every entry to the move queue once and empties its own queue
+        if (cnt[EV_XS_FUEL] != 0u || cnt[EV_ADV] != (unsigned)n)
+            throw std::logic_error("fuel lookup: queue lengths after the launch are wrong");
+        std::vector<uint8_t> seen((size_t)n, 0);
+        for (int64_t i = 0; i < n; ++i) {
+            const int32_t sl = moved[(size_t)i];
+            if (sl < 0 || sl >= n || seen[(size_t)sl]++) throw std::logic_error("fuel lookup: move queue is not a permutation");
+        }
+        for (int64_t i = 0; i < n; ++i) {
+            out[4 * i] = rec[(size_t)i].st;
+            out[4 * i + 1] = rec[(size_t)i].sa;
+            out[4 * i + 2] = rec[(size_t)i].sf;
+            out[4 * i + 3] = rec[(size_t)i].snf;
+        }
+    } catch (...) {
+        cudaStreamDestroy(s);
+        throw;
     }
     cudaStreamDestroy(s);
 }

@@ -22,6 +22,8 @@ void run_transport(const Problem& p, const omcg_run_config& cfg, omcg_run_result
 uint64_t device_hash_build(const Problem& p, int n_bins, int device, int32_t* hash_out);
 void device_xs_lookup(const Problem& p, int n_bins, int device, int64_t n, const int32_t* mat, const double* E,
                       double* out);
+void device_xs_lookup_queue(const Problem& p, int n_bins, int device, int64_t n, const int32_t* mat, const double* E,
+                            int64_t sort_threshold, double* out, double* ckpt_out);
 
 std::vector<int64_t>& last_queue_trace();
 void bank_exchange_plan(const uint64_t* S_all, int world, int64_t n_batch, uint64_t off, int rank, int64_t* plan);

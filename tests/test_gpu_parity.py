@@ -42,15 +42,56 @@ def test_macro_xs_bit_exact(kind, bins):
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
 
 
+@pytest.mark.parametrize("bins", [100, 4000])
+@pytest.mark.parametrize("sort", [None, 20000])
+@pytest.mark.parametrize("mix", ["fuel", "mixed"])
+def test_fuel_lookup_kernel_bit_exact(bins, sort, mix):
+    """The production fuel calculate_xs (k_xs_fuel_fused: 4 warps share the
+    17 segments of the 261-nuclide fuel, partials folded in shared memory) on a
+    queue of 1.2e5 histories, unsorted and sorted by (material, energy) as the
+    queued loop sorts at P3 — macroscopic XS and the 16 segment checkpoints the
+    collision samples from, bit for bit against the oracle."""
+    kind = P.ASSEMBLY
+    o = O.Problem(kind, 1234, bins)
+    p = P.Problem(kind, 1234)
+    rng = np.random.default_rng(7)
+    n = 120_000
+    E = np.exp(rng.uniform(np.log(1e-6), np.log(3e7), n))  # includes out-of-grid energies
+    E[:6] = [1e-5, 2e7, 1e-7, 5e7, 1e-5 * (1 + 1e-15), 2e7 * (1 - 1e-15)]
+    E[6:1000] = E[6]  # one energy many times (a sorted bucket of equal keys)
+    fuel = o.info.fuel_material
+    mat = np.full(n, fuel, np.int32) if mix == "fuel" else rng.integers(0, o.info.n_materials, n).astype(np.int32)
+    got, gck = p.xs_lookup_queue(bins, mat, E, sort_threshold=sort)
+    want, wck, nck = o.macro_ckpt_n(mat, E)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    for k in range(16):
+        sel = nck > k
+        assert np.array_equal(gck[sel, k].view(np.uint64), wck[sel, k].view(np.uint64)), k
+    if mix == "fuel":
+        assert (nck == 16).all()
+
+
+def _oracle_run(kind, n, batches, inactive, rec_n, bins):
+    key = (kind, n, batches, inactive, rec_n, bins)
+    if key not in _ORACLE_CACHE:
+        o = O.Problem(kind, 1234, bins)
+        ores, otally, orecs = o.run(n, batches, inactive, seed=1, record_batch=2, record_n=rec_n)
+        _ORACLE_CACHE[key] = (ores, otally, O.records_array(orecs, rec_n))
+    return _ORACLE_CACHE[key]
+
+
+_ORACLE_CACHE = {}
+
+
 def _compare_runs(kind, n, batches, inactive, rec_n, **kw):
-    o = O.Problem(kind, 1234, kw.get("n_bins", 4000))
-    ores, otally, orecs = o.run(n, batches, inactive, seed=1, record_batch=2, record_n=rec_n)
+    # the oracle's results do not depend on P2 (its hash bracket is repaired
+    # like the GPU's), so one oracle run per problem size serves every variant
+    ores, otally, orec = _oracle_run(kind, n, batches, inactive, rec_n, kw.get("n_bins", 4000))
     p = P.Problem(kind, 1234)
     out = P.run(p, n_particles=n, n_batches=batches, n_inactive=inactive, seed=1, record_batch=2,
                 record_n=rec_n, **kw)
     r = out.result
     assert r.n_lost == ores.n_lost == 0
-    orec = O.records_array(orecs, rec_n)
     for f in ("n_xs", "n_adv", "n_cross", "n_coll", "n_sites", "term"):
         assert np.array_equal(out.records[f], orec[f]), f
     assert np.array_equal(out.records["e_final"].view(np.uint64), orec["e_final"].view(np.uint64))
@@ -98,7 +139,20 @@ def test_queue_contents_bit_exact(kind, n, in_flight, tail, sort, fusion, cap):
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("kw", [
+def test_c2_bench_configuration_bit_exact():
+    """Parity where the benchmark runs (BASELINE.json configs[1], bench.py's
+    defaults): 17x17 assembly, 261-nuclide depleted fuel, 1e6 histories per
+    batch, P1 = 1e6 in flight, P2 = 4000, P3 = 20000 (the fuel-queue sort fires:
+    checked below), queued with event fusion, move cap 20, tail threshold
+    16384 — 3 batches (1 inactive). k per batch, int64 tallies, event totals
+    and the records of the first 1e4 histories of batch 2, bit for bit."""
+    n = 1_000_000
+    out = _compare_runs(P.ASSEMBLY, n, 3, 1, 10_000, particles_in_flight=n, n_bins=4000, sort_threshold=20_000)
+    assert out.result.sorts > 0
+    assert out.result.tail_launches == 3
+
+
+TUNED_VARIANTS = [
     dict(particles_in_flight=1000),                       # P1 < N: dynamic refill
     dict(particles_in_flight=5000, sort_threshold=0),     # always sort
     dict(particles_in_flight=5000, sort_threshold=-1),    # never sort
@@ -123,10 +177,28 @@ def test_queue_contents_bit_exact(kind, n, in_flight, tail, sort, fusion, cap):
     # one history in flight at a time; more slots than histories
     dict(particles_in_flight=1, tail_threshold=0),
     dict(particles_in_flight=50000),
-])
+    # the per-batch exchanges through a one-rank NCCL communicator
+    dict(particles_in_flight=5000, force_nccl=True),
+]
+ASSEMBLY_VARIANTS = TUNED_VARIANTS + [
+    dict(particles_in_flight=10000, sort_threshold=500),  # the sort fires on the depleted fuel queue
+    dict(particles_in_flight=2500, sort_threshold=500, tail_threshold=100),
+    dict(mode="openmc-queueless", particles_in_flight=10000, tasks_per_gpu=2),
+]
+
+
+@pytest.mark.parametrize("kw", TUNED_VARIANTS)
 def test_tuned_parameters_do_not_change_results(kw):
     """in-flight count (and every other tuned knob) changes time only."""
     _compare_runs(P.PINCELL, 10000, 3, 1, 1000, **kw)
+
+
+@pytest.mark.parametrize("kw", [k for k in ASSEMBLY_VARIANTS if k.get("particles_in_flight") != 1])
+def test_tuned_parameters_do_not_change_results_assembly(kw):
+    """The same invariance on the 261-nuclide depleted-fuel assembly (17
+    segments per fuel lookup: the split-K lookup, the collision checkpoints,
+    the fuel-queue sort at P3 = 500 and 0)."""
+    _compare_runs(P.ASSEMBLY, 10000, 3, 1, 1000, **kw)
 
 
 def test_core_transport_bit_exact():
@@ -143,3 +215,21 @@ def test_core_transport_bit_exact():
 def test_tiny_ragged_runs_bit_exact(kw):
     """Edge sizes: fewer histories than ranks x sub-banks, a 2-slot bank."""
     _compare_runs(P.PINCELL, 7, 3, 1, 7, **kw)
+
+
+def test_infinite_medium_bit_exact_vs_oracle():
+    _compare_runs(P.INFINITE, 20000, 3, 1, 1000, particles_in_flight=5000)
+
+
+@pytest.mark.parametrize("mode", ["openmc", "openmc-queueless"])
+def test_infinite_medium_analytic(mode):
+    """Independent physics pin of the GPU path (not through the oracle): the
+    analytic infinite medium at 1e6 histories per batch — k_inf =
+    nu*Sigma_f/Sigma_a within 3 sigma (collision and track-length estimators)
+    and exactly (absorption estimator), Sigma_t/Sigma_a collisions and
+    1/Sigma_a track length per history, no leakage (tests/analytic.py)."""
+    import analytic
+    p = P.Problem("infinite")
+    n, b, i = 1_000_000, 12, 2
+    out = P.run(p, mode=mode, n_particles=n, n_batches=b, n_inactive=i, particles_in_flight=n)
+    analytic.check(out.result, out.tally, n, b, i)

@@ -182,3 +182,14 @@ def test_queue_trace_consistent_with_history_transport(kind):
     t_off = p.queue_trace(n, n, 0, seed=1, event_fusion=True, move_cap=0)
     assert np.array_equal(p.queue_trace(n, n, 0, seed=1, event_fusion=True, move_cap=10**6), t_off)
     assert len(t_c1) > len(t_off)
+
+
+def test_oracle_matches_infinite_medium_analytic():
+    """Independent physics pin of the oracle: the analytic infinite medium
+    (k_inf = nu*Sigma_f/Sigma_a = 1.5625, Sigma_t/Sigma_a collisions and
+    1/Sigma_a track length per history), tests/analytic.py."""
+    import analytic
+    p = O.Problem(O.INFINITE, 1234, 4000)
+    n, b, i = 50_000, 22, 2
+    res, tally, _ = p.run(n, b, i, seed=1, threads=0)
+    analytic.check(res, tally, n, b, i)
