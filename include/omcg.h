@@ -195,6 +195,14 @@ OMCG_API int omcg_run(const omcg_problem* p, const omcg_run_config* cfg, omcg_ru
  * triples (queue id, length, checksum of particle ids). */
 OMCG_API int64_t omcg_queue_trace(int64_t* out, int64_t max_entries);
 
+/* Cumulative GPU energy counter of CUDA device `device` in millijoules (NVML
+ * nvmlDeviceGetTotalEnergyConsumption). The `openmc` front end reads it right
+ * after leasing its GPUs and again at exit, so metrics.txt covers the whole
+ * evaluation process (library generation, upload, hash build, transport,
+ * teardown) like the harness's elapsed time (proj/src/harness.cpp:311-323).
+ * OMCG_EIO when NVML is unavailable. */
+OMCG_API int omcg_energy_counter_mj(int device, uint64_t* mj);
+
 /* NCCL unique id for a multi-process job (rank 0 creates, others receive). */
 OMCG_API int omcg_nccl_unique_id(unsigned char out[128]);
 OMCG_API int omcg_device_count(int* n);

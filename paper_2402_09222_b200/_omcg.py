@@ -25,7 +25,7 @@ EXPORTS = (
     "omcg_problem_get_info", "omcg_library_checksum", "omcg_hash_build", "omcg_xs_lookup",
     "omcg_xs_lookup_queue",
     "omcg_run_config_default", "omcg_run", "omcg_queue_trace", "omcg_nccl_unique_id",
-    "omcg_device_count", "omcg_bank_exchange_plan",
+    "omcg_device_count", "omcg_bank_exchange_plan", "omcg_energy_counter_mj",
 )
 
 
@@ -99,5 +99,6 @@ def load() -> C.CDLL:
     lib.omcg_queue_trace.restype = C.c_int64
     lib.omcg_nccl_unique_id.argtypes = [C.c_void_p]
     lib.omcg_device_count.argtypes = [C.POINTER(C.c_int)]
+    lib.omcg_energy_counter_mj.argtypes = [C.c_int, C.POINTER(C.c_uint64)]
     lib.omcg_bank_exchange_plan.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_int, C.c_void_p]
     return lib

@@ -34,6 +34,9 @@ int wrap(F&& f) {
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return OMCG_EINVAL;
+    } catch (const omcg::IoError& e) {
+        g_err = e.what();
+        return OMCG_EIO;
     } catch (const std::bad_alloc&) {
         g_err = "out of host memory";
         return OMCG_EFAIL;
@@ -169,6 +172,14 @@ OMCG_API int omcg_nccl_unique_id(unsigned char out[128]) {
     });
 }
 
+OMCG_API int omcg_energy_counter_mj(int device, uint64_t* mj) {
+    return wrap([&] {
+        if (!mj) throw std::invalid_argument("null argument");
+        unsigned long long v = 0;
+        if (!omcg::energy_counter_mj(device, &v)) throw omcg::IoError("NVML energy counter unavailable");
+        *mj = (uint64_t)v;
+    });
+}
 OMCG_API int omcg_bank_exchange_plan(const uint64_t* S_all, int world, int64_t n_batch, uint64_t off, int rank,
                                      int64_t* plan) {
     return wrap([&] {

@@ -152,6 +152,11 @@ int main(int argc, char** argv) {
     cfg.n_gpus = want;
     for (int i = 0; i < want; ++i) cfg.devices[i] = gpus[i];
 
+    // energy of the whole evaluation (init included), as the harness's
+    // elapsed covers the whole process (proj/src/harness.cpp:311-323)
+    std::vector<uint64_t> e0(want, 0);
+    bool energy_ok = true;
+    for (int i = 0; i < want; ++i) energy_ok = energy_ok && omcg_energy_counter_mj(gpus[i], &e0[i]) == OMCG_OK;
     auto t0 = std::chrono::steady_clock::now();
     omcg_problem* p = nullptr;
     if (omcg_problem_create(kind, xs_seed, cfg.host_threads, &p) != OMCG_OK) {
@@ -185,13 +190,23 @@ int main(int argc, char** argv) {
                  (long long)res.n_events[2], (long long)res.n_events[3], (long long)res.n_leaked,
                  (long long)res.n_lost, res.t_active, res.t_total, wall, (long long)res.kernel_launches,
                  (long long)res.queue_iterations, (long long)res.sorts, res.energy_j);
-    if (FILE* f = std::fopen("metrics.txt", "w")) {
-        std::fprintf(f, "%.6f %.6f\n", res.energy_j, 0.0);
-        std::fclose(f);
-    }
     std::printf("FOM: %.6e particles/s\n", res.fom);
     std::fflush(stdout);
     omcg_problem_free(p);
+    double joules = 0.0;
+    for (int i = 0; i < want && energy_ok; ++i) {
+        uint64_t e1 = 0;
+        energy_ok = omcg_energy_counter_mj(gpus[i], &e1) == OMCG_OK;
+        joules += (double)(e1 - e0[i]) * 1e-3;
+    }
+    if (!energy_ok) joules = res.energy_j;  // NVML gone mid-run: the transport call's own reading
+    // GPU energy in the package field; DRAM energy is not metered separately (HBM is inside the GPU's reading)
+    if (FILE* f = std::fopen("metrics.txt", "w")) {
+        std::fprintf(f, "%.6f %.6f\n", joules, 0.0);
+        std::fclose(f);
+    }
+    std::fprintf(stderr, "energy %.1f J over %.3f s (GPU, whole evaluation after the lease)\n", joules,
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     for (int fd : fds) ::close(fd);
     return 0;
 }

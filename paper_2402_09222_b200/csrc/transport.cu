@@ -1152,6 +1152,18 @@ Nvml& nvml() {
 }
 }  // namespace
 
+bool energy_counter_mj(int cuda_device, unsigned long long* mj) {
+    Nvml& N = nvml();
+    if (!N.ok) return false;
+    char bus[64];
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, cuda_device) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    void* h = nullptr;
+    return N.by_pci(bus, &h) == 0 && N.energy(h, mj) == 0;
+}
+
 bool EnergyMeter::start(const std::vector<int>& cuda_devices) {
     ok = false;
     handles.clear();

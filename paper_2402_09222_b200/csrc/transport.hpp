@@ -15,6 +15,9 @@ struct CudaError : std::runtime_error {
 struct NcclError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 void run_transport(const Problem& p, const omcg_run_config& cfg, omcg_run_result* res, int64_t* tally_out,
                    omcg_record* records);
@@ -29,6 +32,9 @@ std::vector<int64_t>& last_queue_trace();
 void bank_exchange_plan(const uint64_t* S_all, int world, int64_t n_batch, uint64_t off, int rank, int64_t* plan);
 void nccl_unique_id(unsigned char out[128]);
 int device_count();
+
+// NVML cumulative energy of one CUDA device, mJ (false when unavailable)
+bool energy_counter_mj(int cuda_device, unsigned long long* mj);
 
 // NVML energy counter (dlopen'ed; returns false when unavailable)
 struct EnergyMeter {

@@ -121,3 +121,51 @@ def test_unchanged_reference_campaign_runs_on_gpu_edp(tmp_path):
     r, rows = run_campaign(str(cj), tmp_path / "edp", 4, 2, SMALL)
     assert r.returncode == 0, r.stderr
     assert all(row["status"] == "ok" and float(row["objective"]) > 0 for row in rows), rows
+
+
+def _abs_campaign(tmp_path, name, **overrides):
+    src = json.load(open(CAMPAIGN))
+    d = os.path.dirname(CAMPAIGN)
+    for k in ("space_file", "mold_file", "launcher_file"):
+        src[k] = os.path.join(d, src[k])
+    src.pop("baseline", None)
+    src.update(overrides)
+    cj = tmp_path / name
+    cj.write_text(json.dumps(src))
+    return str(cj)
+
+
+@have_ref
+@pytest.mark.gpu
+def test_timeout_sigkill_releases_gpu_lease(tmp_path):
+    """The harness SIGKILLs the whole process group at the timeout with no
+    grace period (proj/src/harness.cpp:267-283). A killed bin/openmc must leave
+    no state behind: its flock GPU lease is released by the kernel, no process
+    of the evaluation survives, and the next evaluations lease the GPU and
+    finish ok."""
+    import fcntl
+    lease = tmp_path / "lease"
+    lease.mkdir()
+    # long runs (1e6 histories x 40 batches, ~3 s on the GPU) against a 1.5 s timeout
+    killer = _abs_campaign(tmp_path, "timeout.json", timeout=1.5)
+    big = {"OMCG_PARTICLES": "1000000", "OMCG_BATCHES": "40", "OMCG_INACTIVE": "1", "OMCG_LEASE_DIR": str(lease)}
+    r, rows = run_campaign(killer, tmp_path / "killed", 3, 1, big)
+    assert r.returncode == 0, r.stderr
+    assert [row["status"] for row in rows] == ["timeout"] * 3, rows
+    for row in rows:  # the binary was inside its GPU run when it was killed (it had leased the GPU)
+        err = open(tmp_path / "killed" / "evals" / row["eval_id"] / "stdout.log").read()
+        assert "FOM:" not in err
+    # no holder of the lease survives the SIGKILL
+    fd = os.open(str(lease / "omcg-gpu-0.lock"), os.O_RDWR)
+    try:
+        fcntl.flock(fd, fcntl.LOCK_EX | fcntl.LOCK_NB)  # raises if any process still holds it
+        fcntl.flock(fd, fcntl.LOCK_UN)
+    finally:
+        os.close(fd)
+    ps = subprocess.run(["ps", "-eo", "comm="], capture_output=True, text=True).stdout.split()
+    assert not any(c.startswith("openmc") for c in ps), ps
+    # the next evaluations lease the same GPU and complete
+    ok = _abs_campaign(tmp_path, "ok.json")
+    r, rows = run_campaign(ok, tmp_path / "after", 3, 2, dict(SMALL, OMCG_LEASE_DIR=str(lease)))
+    assert r.returncode == 0, r.stderr
+    assert all(row["status"] == "ok" and float(row["objective"]) > 0 for row in rows), rows
