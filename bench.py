@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--tail", type=int, default=None, help="tail threshold (histories; default: library default)")
     ap.add_argument("--cpu-sample", type=int, default=100_000, help="histories per CPU-baseline batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-nccl", action="store_true",
+                    help="per-batch exchanges through NCCL even at one rank (one-rank communicator)")
+    ap.add_argument("--no-policy-line", action="store_true",
+                    help="skip the short one-kernel-per-event (paper P0 policy) measurement")
     return ap.parse_args()
 
 
@@ -209,14 +213,35 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic_per_item():
-    """dram bytes per fuel-XS queue entry from the committed ncu --set full capture."""
+def ncu_roofs():
+    """Per-kernel counters of the committed ncu --set full captures
+    (profiles/roofline_ncu.json, written by scripts/ncu_summary.py): DRAM bytes
+    per work item and the binding on-chip roofs (L1/TEX throughput, issue
+    active, lanes per instruction, warps per SM)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "xs_fuel_ncu.json")) as f:
-            d = json.load(f)
-        return float(d["dram_bytes_per_item"]), d.get("source", "profiles/xs_fuel_ncu.json")
-    except (OSError, KeyError, ValueError):
-        return None, None
+        with open(os.path.join(ROOT, "profiles", "roofline_ncu.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def roof_fields(k, items, ms, peak):
+    """DRAM rate of a kernel class from the ncu bytes per item x the items it
+    processed in the timed region / its CUDA-event time, as a fraction of the
+    HBM peak, next to the roof that binds it (ncu percent of peak)."""
+    if not k:
+        return {}
+    per = k.get("dram_bytes_per_item")
+    # items known per capture (fuel lookups): bytes per item x the timed region's items / its time;
+    # otherwise (persistent move kernel) the captured launch's own DRAM rate
+    dram = per * items / (ms * 1e-3) / 1e9 if per and items and ms else k.get("dram_gbs")
+    return {"dram_bytes_per_item": per, "dram_achieved_gbs": dram,
+            "dram_frac": dram / peak if dram else None,
+            "binding_roof": {"name": k.get("binding"), "l1tex_throughput_pct": k.get("l1tex_pct"),
+                             "issue_active_pct": k.get("issue_active_pct"),
+                             "lanes_per_instruction": k.get("lanes_per_inst"),
+                             "warps_per_sm": k.get("warps_per_sm"), "l2_hit_pct": k.get("l2_hit_pct"),
+                             "ncu_items_in_capture": k.get("items"), "source": k.get("source")}}
 
 
 def cpu_baseline(a, batches=3, inactive=1):
@@ -239,22 +264,32 @@ def run_reference(a, rank):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     kind = {"pincell": O.PINCELL, "assembly": O.ASSEMBLY, "core": O.CORE}[a.problem]
+    # a bounded sample of the workload: the same problem, library, seeds and
+    # tuned parameters, but n histories per batch (a full 1e6-history batch
+    # takes ~15 s per batch on the host cores); the line says what ran
     n = max(1000, a.cpu_sample // 2)
     p = O.Problem(kind, 1234, a.bins)
     t0 = time.perf_counter()
     res, _, _ = p.run(n, a.warmup + a.steps, a.warmup, seed=1, threads=0)
     wall = time.perf_counter() - t0
     cores = os.cpu_count()
+    cfg = workload_config(a, 1)
+    cfg["workload"] = (f"{a.problem} (the C2 problem of the GPU arm), bounded sample: {n} histories/batch "
+                       f"instead of {a.particles}")
+    cfg["histories_per_batch"] = n
+    cfg["sample_of"] = workload_config(a, 1)["workload"]
     line = {
         "impl": "reference", "metric": METRIC, "value": res.fom, "unit": "particles/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * res.t_active / a.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded library xs_seed=1234, transport seed=1)",
-        "config": workload_config(a, 1),
+        "config": cfg,
         "cpu_baseline": {"value": res.fom, "unit": "particles/s", "cores": cores, "kind": "port",
-                         "sample": f"{n} histories/batch x {a.warmup + a.steps} batches on the host CPU "
-                                   "(the reference ships no transport code; this is the CPU oracle port, "
-                                   "oracle/omc_oracle.c)"},
+                         "sample": f"{n} histories/batch x {a.warmup + a.steps} batches ({a.warmup} inactive) on "
+                                   f"{cores} host threads: the CPU oracle port (oracle/omc_oracle.c), "
+                                   "history-based (one thread follows one history through all its events); "
+                                   "the reference ships no transport code, and FoM per history is "
+                                   "independent of the batch size on the CPU"},
         "e2e": {"value": res.fom, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "k_eff": res.k_mean, "wall_s": wall,
     }
@@ -278,11 +313,12 @@ def main():
     import paper_2402_09222_b200 as P
 
     problem = P.Problem(a.problem, host_threads=8)  # host buffers: the e2e inputs
-    nccl_id = warm_id = None
-    if world > 1:  # one NCCL unique id per omcg_run call (each call builds its own communicator)
-        obj = [(P.nccl_unique_id(), P.nccl_unique_id()) if rank == 0 else None]
+    nccl_id = None
+    if world > 1:  # one NCCL unique id: the library builds the communicator in the warm-up call and reuses it
+        obj = [P.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        warm_id, nccl_id = obj[0]
+        nccl_id = obj[0]
+    warm_id = nccl_id
     sampler = clock_sampler(local) if rank == 0 else None
     # untimed warm-up call of the same configuration (one batch): loads the
     # kernels (lazy module loading) and lets the device memory pool reach its
@@ -291,7 +327,8 @@ def main():
     P.run(problem, mode=a.mode, particles_in_flight=a.in_flight, n_bins=a.bins,
           sort_threshold=a.sort if a.mode == "openmc" else None, host_threads=8, tasks_per_gpu=a.tasks,
           n_particles=a.particles * world, n_batches=1, n_inactive=0, seed=7, world_size=world, rank=rank,
-          nccl_id=warm_id, devices=[local], event_fusion=a.event_fusion, tail_threshold=a.tail)
+          nccl_id=warm_id, devices=[local], event_fusion=a.event_fusion, tail_threshold=a.tail,
+          force_nccl=a.force_nccl)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -303,7 +340,7 @@ def main():
                 sort_threshold=a.sort if a.mode == "openmc" else None, host_threads=8, tasks_per_gpu=a.tasks,
                 n_particles=a.particles * world, n_batches=a.warmup + a.steps, n_inactive=a.warmup, seed=1,
                 world_size=world, rank=rank, nccl_id=nccl_id, devices=[local], profile=2,
-                event_fusion=a.event_fusion, tail_threshold=a.tail)
+                event_fusion=a.event_fusion, tail_threshold=a.tail, force_nccl=a.force_nccl)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     clocks = sampler.stop() if sampler else None
@@ -318,6 +355,18 @@ def main():
                  "sort", "refill", "tail"]
         tot = sum(pr.prof_ms[i] for i in range(8))
         shares = {names[i]: round(pr.prof_ms[i] / tot, 4) for i in range(8)} if tot else None
+    # the paper's P0 policy taken literally: one kernel per
+    # event type and the longest of the per-event queues each iteration
+    # (event_fusion = 0); same histories and results, a short separate pass
+    policy = None
+    if world == 1 and a.mode == "openmc" and a.event_fusion == 1 and not a.no_policy_line:
+        pe = P.run(problem, mode=a.mode, particles_in_flight=a.in_flight, n_bins=a.bins, sort_threshold=a.sort,
+                   host_threads=8, tasks_per_gpu=a.tasks, n_particles=a.particles, n_batches=3, n_inactive=1,
+                   seed=1, devices=[local], event_fusion=0, tail_threshold=a.tail).result
+        policy = {"fom": pe.fom, "event_fusion": 0, "batches": "1 inactive + 2 active",
+                  "queue_iterations_per_batch": pe.queue_iterations / 3,
+                  "what": "paper-literal P0 queued policy: one kernel per event type (calculate_xs fuel / "
+                          "non-fuel, advance, surface_crossing, collision), longest queue first"}
     if world > 1:
         t = torch.tensor([wall], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -332,7 +381,9 @@ def main():
     peak, peak_src = peaks()
     xs_ms = r.prof_ms[0]
     achieved = (r.xs_fuel_bytes / (xs_ms * 1e-3) / 1e9) if xs_ms > 0 else None
-    per_item, traffic_src = ncu_traffic_per_item()
+    roofs = ncu_roofs()
+    kx = roofs.get("k_xs_fuel_fused", {})
+    per_item = kx.get("dram_bytes_per_item")
     items_per_launch = r.prof_items[0] / max(1, r.prof_launches[0])
     line = {
         "metric": METRIC, "value": r.fom, "unit": "particles/s", "n_gpus": world, "steps": a.steps,
@@ -346,13 +397,26 @@ def main():
                 "what": "omcg_run through the C ABI from host buffers: library upload + hash build + all "
                         f"{a.warmup + a.steps} batches + result readback, wall clock (max over ranks), "
                         "after one untimed warm-up call in the same process"},
-        "roofline": {"bound": "hbm", "kernel": "calculate_xs (fuel queue)",
+        # calculate_xs (fuel queue, k_xs_fuel_fused): `achieved`/`frac` count the
+        # ALGORITHMIC bytes (44 + 100 x 261 per lookup) per
+        # CUDA-event second, so sorted reuse in L1/L2 lifts them above 1; the
+        # DRAM bytes actually moved (ncu) and the roof that binds the kernel
+        # (L1/TEX throughput) are reported beside them
+        "roofline": {"bound": "hbm", "kernel": "calculate_xs (fuel queue, k_xs_fuel_fused)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": (per_item * items_per_launch) if per_item else None,
                      "algorithmic_bytes_per_lookup": 44 + 100 * FUEL_NUCLIDES,
                      "items_per_launch": items_per_launch, "launches": r.prof_launches[0],
-                     "peak_source": peak_src, "traffic_source": traffic_src},
+                     "peak_source": peak_src,
+                     **roof_fields(kx, r.prof_items[0], xs_ms, peak)},
+        # the move kernel (advance + surface crossing + non-fuel calculate_xs in
+        # registers): divergent, bound by issue / latency, not by DRAM
+        "roofline_move": ({"kernel": "k_move", "share_of_kernel_time": shares.get("advance") if shares else None,
+                           "ms_per_batch": pr.prof_ms[2] / 2 if world == 1 else None,
+                           **roof_fields(roofs.get("k_move"), pr.prof_items[2], pr.prof_ms[2], peak)}
+                          if world == 1 else None),
+        "policy_one_kernel_per_event": policy,
         "kernel_share": shares,
         "kernel_share_note": "CUDA-event time per kernel class from a separate 1+2-batch pass with every launch "
                              "timed; the timed run above times only the fuel calculate_xs launches",

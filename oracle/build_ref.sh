@@ -46,4 +46,14 @@ if [ ! -f "$stamp" ] || [ -n "$(find "$R/src" "$HERE/ref_rng_shim.cpp" "$HERE/at
     cp -r "$R/campaigns" "$OUT/campaigns"
     touch "$stamp"
 fi
+# the reference's campaign loop with this repo's in-process GPU evaluator
+# (integration/, a third EvaluatorKind by composition; links libomcg.so)
+ROOT="$(cd "$HERE/.." && pwd)"
+LIBOMCG="$ROOT/paper_2402_09222_b200/libomcg.so"
+if [ -f "$LIBOMCG" ] && { [ ! -f "$OUT/atune_gpu_campaign" ] || [ -n "$(find "$ROOT/integration" "$LIBOMCG" "$stamp" -newer "$OUT/atune_gpu_campaign" 2>/dev/null | head -1)" ]; }; then
+    $CXX $FLAGS -I"$ROOT/include" -I"$ROOT/integration" -o "$OUT/atune_gpu_campaign" \
+        "$ROOT/integration/atune_gpu_campaign.cpp" "$ROOT/integration/gpu_evaluator.cpp" "$OUT"/obj/*.o \
+        -L"$ROOT/paper_2402_09222_b200" -lomcg -lpthread \
+        -Wl,-rpath,'$ORIGIN/../../paper_2402_09222_b200'
+fi
 echo "build_ref: $OUT ready"

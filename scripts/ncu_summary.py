@@ -81,6 +81,30 @@ def main():
         json.dump({"dram_bytes_per_item": per, "kernels": parts,
                    "source": f"profiles/{tag}_ncu_summary.json ({'+'.join(xs_kernels)}, cold cache)"},
                   open(os.path.join(prof, "xs_fuel_ncu.json"), "w"), indent=1)
+    # roofs per kernel for bench.py (profiles/roofline_ncu.json)
+    roofs = {}
+    for k, x in summary.items():
+        base = k.split("@")[0]
+        if base not in ("k_xs_fuel_fused", "k_move", "k_collide", "k_tail_warp"):
+            continue
+        dram = x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0)
+        t = x.get("gpu__time_duration.sum")
+        l1 = x.get("l1tex__throughput.avg.pct_of_peak_sustained_active")
+        issue = x.get("smsp__issue_active.avg.pct_of_peak_sustained_active")
+        d = {"binding": "L1/TEX throughput" if (l1 or 0) >= (issue or 0) else "issue (latency-bound warps)",
+             "l1tex_pct": l1, "issue_active_pct": issue,
+             "lanes_per_inst": x.get("smsp__thread_inst_executed_per_inst_executed.ratio"),
+             "warps_per_sm": x.get("sm__warps_active.avg.per_cycle_active"),
+             "l2_hit_pct": x.get("lts__t_sector_hit_rate.pct"),
+             "dram_gbs": dram / t / 1e9 if t else None, "ms": 1e3 * t if t else None,
+             "source": f"profiles/{tag}_ncu_summary.json ({k}, ncu --set full, cold cache)"}
+        if base == "k_xs_fuel_fused":
+            d["items"] = x["launch__grid_size"] * 32  # 32 fuel lookups per block
+            d["dram_bytes_per_item"] = dram / d["items"]
+        if base not in roofs or (d.get("items", 0) > roofs[base].get("items", 0)) or base != "k_xs_fuel_fused":
+            roofs[base] = d
+    if roofs:
+        json.dump(roofs, open(os.path.join(prof, "roofline_ncu.json"), "w"), indent=1)
     lc = os.path.join(src, "launches.csv")
     if os.path.exists(lc):
         rows = list(csv.reader(open(lc)))

@@ -12,6 +12,9 @@ if os.environ.get("PHASE_CHILD") != "1":
         cur.append((int(c), int(it), ms))
         if c == 7:
             batches.append(cur); cur = []
+    import json
+    os.makedirs("gpurun_out", exist_ok=True)
+    json.dump({"classes": names, "batches": batches[-2:]}, open("gpurun_out/phase_launches.json", "w"))
     for b in batches[-2:]:
         tot = sum(x[2] for x in b)
         last_refill = max(i for i, x in enumerate(b) if x[0] == 6)

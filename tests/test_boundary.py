@@ -169,3 +169,43 @@ def test_timeout_sigkill_releases_gpu_lease(tmp_path):
     r, rows = run_campaign(ok, tmp_path / "after", 3, 2, dict(SMALL, OMCG_LEASE_DIR=str(lease)))
     assert r.returncode == 0, r.stderr
     assert all(row["status"] == "ok" and float(row["objective"]) > 0 for row in rows), rows
+
+
+GPU_CAMPAIGN = os.path.join(REF, "atune_gpu_campaign")
+have_gpu_campaign = pytest.mark.skipif(not os.path.exists(GPU_CAMPAIGN),
+                                       reason="in-process GPU evaluator driver not built (oracle/build_ref.sh)")
+
+
+def run_gpu_campaign(campaign, out, evals, workers, env):
+    e = dict(os.environ)
+    e.update(env)
+    r = subprocess.run([GPU_CAMPAIGN, campaign, str(out), str(evals), str(workers)], capture_output=True,
+                       text=True, env=e, timeout=1800)
+    return r, read_results(os.path.join(out, "results.csv"))
+
+
+@have_gpu_campaign
+@pytest.mark.skipif(has_gpu(), reason="GPU visible")
+def test_inprocess_gpu_evaluator_failures_without_gpu(tmp_path):
+    """The in-process evaluator (integration/gpu_evaluator.cpp) under the
+    reference's own campaign loop: without a device every evaluation is
+    status fail with the penalty, and the campaign still completes."""
+    r, rows = run_gpu_campaign(CAMPAIGN, tmp_path / "g", 4, 2, {})
+    assert r.returncode == 0, r.stderr
+    assert len(rows) == 4 and all(row["status"] == "fail" and float(row["objective"]) == -1.0 for row in rows)
+
+
+@have_gpu_campaign
+@pytest.mark.gpu
+@pytest.mark.parametrize("metric", ["fom", "edp"])
+def test_inprocess_gpu_evaluator_campaign(tmp_path, metric):
+    """A 4-worker campaign over the unchanged campaigns/openmc space through the
+    in-process `gpu` evaluator kind: the reference's
+    run_campaign calls the evaluator from 4 threads at once; every evaluation
+    leases the GPU in-process and succeeds."""
+    camp = CAMPAIGN if metric == "fom" else _abs_campaign(tmp_path, "edp.json", metric={"kind": "edp"})
+    small = {"OMCG_PARTICLES": "20000", "OMCG_BATCHES": "3", "OMCG_INACTIVE": "1"}
+    r, rows = run_gpu_campaign(camp, tmp_path / metric, 12, 4, small)
+    assert r.returncode == 0, r.stderr
+    assert len(rows) == 12 and all(row["status"] == "ok" and float(row["objective"]) > 0 for row in rows), rows
+    assert len({row["worker_id"] for row in rows}) == 4
