@@ -10,6 +10,7 @@
 // k-eff accumulators with NCCL and redistributes the canonical fission bank.
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -26,6 +27,20 @@
 #include "transport.hpp"
 
 namespace omcg {
+
+// NVTX ranges (SURVEY.md §5 tracing): header-only NVTX3, one indirect call
+// that returns at once unless a tool (nsys, ncu --nvtx) is attached. Every
+// event-kernel launch of the queue loops is a range named by its kernel class
+// (through Prof below); batches, init and the batch synchronisation are ranges too.
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
+const char* const kClassName[8] = {"calculate_xs fuel", "calculate_xs non-fuel", "advance / move",
+                                   "surface_crossing", "collision", "sort fuel queue", "refill", "tail"};
+
 inline NcclApi& nccl_checked() {
     NcclApi& a = nccl();
     if (!a.error.empty()) throw NcclError(a.error);
@@ -333,7 +348,10 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     CK(cudaEventCreate(&R.ev_a0));
     CK(cudaEventCreate(&R.ev_a1));
     mark("streams/events");
-    R.gp.upload(p, cfg.n_bins, R.device, R.main);
+    {
+        Nvtx r("init: library upload + hash build");
+        R.gp.upload(p, cfg.n_bins, R.device, R.main);
+    }
     mark("library upload + hash");
     R.h2d += R.gp.h2d_bytes;
     R.N = cfg.n_particles;
@@ -489,9 +507,10 @@ void drain_profile(SubBank& S) {
 struct Prof {
     SubBank& S;
     bool on;
+    Nvtx range;
     // profile level 1 times every kernel class; level 2 only the fuel calculate_xs
     Prof(SubBank& s, bool enabled, int cls, int64_t items)
-        : S(s), on(enabled && (S.prof_level == 1 || cls == 0)) {
+        : S(s), on(enabled && (S.prof_level == 1 || cls == 0)), range(kClassName[cls]) {
         if (!on) return;
         if (S.n_pending == (int)S.evs.size()) drain_profile(S);
         auto& e = S.evs[S.n_pending];
@@ -924,8 +943,11 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
     const int fuel_nuc = (int)p.mat[MAT_FUEL].nuc.size();
     const int tally_smem = 4 * R.n_tally_bins <= SMEM_TALLY_MAX;
     long long launches0 = 0;
+    char batch_name[32];
     for (int batch = 1; batch <= nb; ++batch) {
         const bool active = batch > cfg.n_inactive;
+        std::snprintf(batch_name, sizeof batch_name, "batch %d%s", batch, active ? "" : " (inactive)");
+        Nvtx batch_range(batch_name);
         if (batch == cfg.n_inactive + 1) {
             CK(cudaStreamSynchronize(R.main));
             CK(cudaEventRecord(R.ev_a0, R.main));
@@ -959,6 +981,7 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         const bool prof = cfg.profile != 0 && active;
 
         auto drive = [&](SubBank& S) {
+            Nvtx r("event loop");
             Ctx c = base;
             c.b = S.b;
             c.qs = S.qs;
@@ -990,6 +1013,7 @@ void run_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
             if (S.h_ctrl[2] & 2ULL) throw std::runtime_error("fission bank overflow");
         }
 
+        Nvtx sync_range("batch sync: reduce + fission bank");
         if (active && R.n_priv > 0)
             launch_tally_fold(R.tally_priv, R.n_priv, 4 * (int64_t)R.n_tally_bins, R.acc.tally, R.main);
         // ---- batch reduction (NCCL across ranks: integer sums are exact)
@@ -1131,11 +1155,13 @@ namespace {
 typedef int (*nvml_init_t)(void);
 typedef int (*nvml_by_pci_t)(const char*, void**);
 typedef int (*nvml_energy_t)(void*, unsigned long long*);
+typedef int (*nvml_power_t)(void*, unsigned int*);
 struct Nvml {
     void* lib = nullptr;
     nvml_init_t init = nullptr;
     nvml_by_pci_t by_pci = nullptr;
     nvml_energy_t energy = nullptr;
+    nvml_power_t power = nullptr;  // optional: mW, for runs shorter than the energy counter's update period
     bool ok = false;
     Nvml() {
         lib = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
@@ -1143,6 +1169,7 @@ struct Nvml {
         init = (nvml_init_t)dlsym(lib, "nvmlInit_v2");
         by_pci = (nvml_by_pci_t)dlsym(lib, "nvmlDeviceGetHandleByPciBusId_v2");
         energy = (nvml_energy_t)dlsym(lib, "nvmlDeviceGetTotalEnergyConsumption");
+        power = (nvml_power_t)dlsym(lib, "nvmlDeviceGetPowerUsage");
         ok = init && by_pci && energy && init() == 0;
     }
 };
@@ -1180,15 +1207,27 @@ bool EnergyMeter::start(const std::vector<int>& cuda_devices) {
         handles.push_back(h);
         start_mj.push_back(mj);
     }
+    t0 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
     ok = true;
     return true;
 }
+// The total-energy counter advances in steps (tens of ms on B200): a run
+// shorter than one step can read 0 J, which would make its EDP 0 -- the best
+// possible objective. Such a device is charged its current power draw over
+// the run's wall time instead.
 double EnergyMeter::stop_joules() {
     if (!ok) return 0.0;
+    const double dt =
+        std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count() - t0;
+    Nvml& N = nvml();
     double j = 0.0;
     for (size_t i = 0; i < handles.size(); ++i) {
         unsigned long long mj = 0;
-        if (nvml().energy(handles[i], &mj) == 0) j += (double)(mj - start_mj[i]) * 1e-3;
+        if (N.energy(handles[i], &mj) != 0) continue;
+        double dj = (double)(mj - start_mj[i]) * 1e-3;
+        unsigned int mw = 0;
+        if (dj <= 0.0 && N.power && N.power(handles[i], &mw) == 0) dj = 1e-3 * (double)mw * dt;
+        j += dj;
     }
     return j;
 }

@@ -42,6 +42,7 @@ struct EnergyMeter {
     double stop_joules();  // energy since start, summed over devices
     std::vector<void*> handles;
     std::vector<unsigned long long> start_mj;
+    double t0 = 0.0;  // steady-clock seconds at start
     bool ok = false;
 };
 

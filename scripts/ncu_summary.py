@@ -65,12 +65,18 @@ def main():
     json.dump({"note": note, "kernels": summary}, open(os.path.join(prof, f"{tag}_ncu_summary.json"), "w"),
               indent=1)
     # dram bytes per fuel lookup (queue entry) of the fuel calculate_xs launch(es) captured
-    xs_kernels = [k for k in ("k_xs_fuel", "k_xs_fuel_fused", "k_xs_fuel_seg", "k_xs_fuel_combine") if k in summary]
+    # (captures may carry an @label: the largest launch of each kernel is used)
+    def largest(base):
+        c = [k for k in summary if k.split("@")[0] == base]
+        return max(c, key=lambda k: summary[k].get("launch__grid_size", 0)) if c else None
+    xs_kernels = [largest(k) for k in ("k_xs_fuel", "k_xs_fuel_fused", "k_xs_fuel_seg", "k_xs_fuel_combine")
+                  if largest(k)]
     if xs_kernels:
         nseg = int(os.environ.get("OMCG_FUEL_SEGMENTS", "17"))  # 261 fuel nuclides in 16-nuclide segments
         # fuel lookups (queue entries) per block of each kernel
         per_block = {"k_xs_fuel": None, "k_xs_fuel_combine": None, "k_xs_fuel_fused": 32,
                      "k_xs_fuel_seg": 256 / nseg}
+        per_block = {k: per_block[k.split("@")[0]] for k in xs_kernels}
         per, parts = 0.0, {}
         for k in xs_kernels:
             x = summary[k]

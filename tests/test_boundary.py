@@ -12,6 +12,7 @@ import csv
 import json
 import os
 import subprocess
+import time
 
 import pytest
 
@@ -155,15 +156,29 @@ def test_timeout_sigkill_releases_gpu_lease(tmp_path):
     for row in rows:  # the binary was inside its GPU run when it was killed (it had leased the GPU)
         err = open(tmp_path / "killed" / "evals" / row["eval_id"] / "stdout.log").read()
         assert "FOM:" not in err
-    # no holder of the lease survives the SIGKILL
-    fd = os.open(str(lease / "omcg-gpu-0.lock"), os.O_RDWR)
-    try:
-        fcntl.flock(fd, fcntl.LOCK_EX | fcntl.LOCK_NB)  # raises if any process still holds it
-        fcntl.flock(fd, fcntl.LOCK_UN)
-    finally:
-        os.close(fd)
-    ps = subprocess.run(["ps", "-eo", "comm="], capture_output=True, text=True).stdout.split()
-    assert not any(c.startswith("openmc") for c in ps), ps
+    # No holder of the lease survives the SIGKILL. The harness reaps the
+    # evaluation's /bin/sh at once, while the killed bin/openmc (its child, in
+    # the same process group) may still be tearing down its CUDA context; its
+    # descriptors -- the flock lease among them -- close when that exit
+    # completes. So the contract is "released once the killed processes are
+    # gone", checked with a bounded wait.
+    deadline = time.time() + 30.0
+    while True:
+        ps = subprocess.run(["ps", "-eo", "comm="], capture_output=True, text=True).stdout.split()
+        alive = [c for c in ps if c.startswith("openmc")]
+        fd = os.open(str(lease / "omcg-gpu-0.lock"), os.O_RDWR)
+        try:
+            fcntl.flock(fd, fcntl.LOCK_EX | fcntl.LOCK_NB)  # raises if any process still holds it
+            fcntl.flock(fd, fcntl.LOCK_UN)
+            held = False
+        except BlockingIOError:
+            held = True
+        finally:
+            os.close(fd)
+        if not alive and not held:
+            break
+        assert time.time() < deadline, f"lease held={held}, surviving processes {alive} 30 s after the kill"
+        time.sleep(0.1)
     # the next evaluations lease the same GPU and complete
     ok = _abs_campaign(tmp_path, "ok.json")
     r, rows = run_campaign(ok, tmp_path / "after", 3, 2, dict(SMALL, OMCG_LEASE_DIR=str(lease)))
@@ -207,5 +222,6 @@ def test_inprocess_gpu_evaluator_campaign(tmp_path, metric):
     small = {"OMCG_PARTICLES": "20000", "OMCG_BATCHES": "3", "OMCG_INACTIVE": "1"}
     r, rows = run_gpu_campaign(camp, tmp_path / metric, 12, 4, small)
     assert r.returncode == 0, r.stderr
-    assert len(rows) == 12 and all(row["status"] == "ok" and float(row["objective"]) > 0 for row in rows), rows
+    assert len(rows) == 12 and all(row["status"] == "ok" and float(row["objective"]) > 0 for row in rows), \
+        [(row["status"], row["objective"], row.get("elapsed")) for row in rows]
     assert len({row["worker_id"] for row in rows}) == 4
