@@ -203,6 +203,25 @@ OMCG_API int64_t omcg_queue_trace(int64_t* out, int64_t max_entries);
  * OMCG_EIO when NVML is unavailable. */
 OMCG_API int omcg_energy_counter_mj(int device, uint64_t* mj);
 
+/* Energy metering of a whole evaluation process. omcg_energy_mark() reads the
+ * energy counter of every GPU NVML sees without initialising CUDA; the
+ * `openmc` front end calls it first thing in main(), so that CUDA start-up,
+ * library generation, upload, transport and teardown are all metered, like
+ * the harness's elapsed time, which spans the whole process
+ * (proj/src/harness.cpp:311-323). omcg_energy_since_mark_j() is the energy of
+ * CUDA device `device` since the mark, in J. OMCG_EIO when NVML is
+ * unavailable or no mark was taken. */
+OMCG_API int omcg_energy_mark(void);
+OMCG_API int omcg_energy_since_mark_j(int device, double* joules);
+
+/* End of a process's GPU work: returns the pooled device memory and pinned
+ * host words the library keeps between runs and destroys the CUDA contexts
+ * of the devices it used, so that the `openmc` front end's teardown is metered
+ * (it calls this before its final energy reading) instead of happening in the
+ * process exit. No other omcg call may be in flight; problems stay valid and
+ * later runs initialise the devices again. */
+OMCG_API int omcg_release_devices(void);
+
 /* NCCL unique id for a multi-process job (rank 0 creates, others receive). */
 OMCG_API int omcg_nccl_unique_id(unsigned char out[128]);
 OMCG_API int omcg_device_count(int* n);

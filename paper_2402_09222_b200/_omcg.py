@@ -26,6 +26,7 @@ EXPORTS = (
     "omcg_xs_lookup_queue",
     "omcg_run_config_default", "omcg_run", "omcg_queue_trace", "omcg_nccl_unique_id",
     "omcg_device_count", "omcg_bank_exchange_plan", "omcg_energy_counter_mj",
+    "omcg_energy_mark", "omcg_energy_since_mark_j", "omcg_release_devices",
 )
 
 
@@ -100,5 +101,6 @@ def load() -> C.CDLL:
     lib.omcg_nccl_unique_id.argtypes = [C.c_void_p]
     lib.omcg_device_count.argtypes = [C.POINTER(C.c_int)]
     lib.omcg_energy_counter_mj.argtypes = [C.c_int, C.POINTER(C.c_uint64)]
+    lib.omcg_energy_since_mark_j.argtypes = [C.c_int, C.POINTER(C.c_double)]
     lib.omcg_bank_exchange_plan.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_int, C.c_void_p]
     return lib

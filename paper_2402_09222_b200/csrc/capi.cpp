@@ -180,6 +180,21 @@ OMCG_API int omcg_energy_counter_mj(int device, uint64_t* mj) {
         *mj = (uint64_t)v;
     });
 }
+OMCG_API int omcg_release_devices(void) {
+    return wrap([&] { omcg::release_devices(); });
+}
+OMCG_API int omcg_energy_mark(void) {
+    return wrap([&] {
+        if (!omcg::energy_mark()) throw omcg::IoError("NVML energy counters unavailable");
+    });
+}
+OMCG_API int omcg_energy_since_mark_j(int device, double* joules) {
+    return wrap([&] {
+        if (!joules) throw std::invalid_argument("null argument");
+        if (!omcg::energy_since_mark_j(device, joules))
+            throw omcg::IoError("no NVML energy mark for this device (omcg_energy_mark not called, or NVML unavailable)");
+    });
+}
 OMCG_API int omcg_bank_exchange_plan(const uint64_t* S_all, int world, int64_t n_batch, uint64_t off, int rank,
                                      int64_t* plan) {
     return wrap([&] {

@@ -88,9 +88,43 @@ void bind_cpus(int bind, int threads) {
     sched_setaffinity(0, sizeof set, &set);
 }
 
+// Seconds from this process's creation (/proc/self/stat field 22, clock
+// ticks) to now -- exec and dynamic loading before main -- to 10 ms; -1 when
+// unavailable.
+double seconds_since_process_start() {
+    FILE* f = std::fopen("/proc/self/stat", "r");
+    if (!f) return -1.0;
+    char buf[1024];
+    const size_t n = std::fread(buf, 1, sizeof buf - 1, f);
+    std::fclose(f);
+    buf[n] = 0;
+    const char* p = std::strrchr(buf, ')');  // the command name may contain spaces
+    if (!p) return -1.0;
+    unsigned long long start = 0;
+    int field = 2;
+    for (const char* q = p + 1; *q; ++q)
+        if (*q == ' ' && ++field == 22) {
+            start = std::strtoull(q + 1, nullptr, 10);
+            break;
+        }
+    double up = 0.0;
+    if (FILE* u = std::fopen("/proc/uptime", "r")) {
+        if (std::fscanf(u, "%lf", &up) != 1) up = 0.0;
+        std::fclose(u);
+    }
+    const long tck = sysconf(_SC_CLK_TCK);
+    if (start == 0 || up <= 0.0 || tck <= 0) return -1.0;
+    return up - (double)start / (double)tck;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
+    // the evaluation's energy and wall time start here, before CUDA is
+    // initialised: the harness's elapsed spans the whole process
+    const auto t_proc = std::chrono::steady_clock::now();
+    const double pre_main = seconds_since_process_start();
+    const bool marked = omcg_energy_mark() == OMCG_OK;
     const char* base = std::strrchr(argv[0], '/');
     base = base ? base + 1 : argv[0];
     omcg_run_config cfg;
@@ -152,11 +186,13 @@ int main(int argc, char** argv) {
     cfg.n_gpus = want;
     for (int i = 0; i < want; ++i) cfg.devices[i] = gpus[i];
 
-    // energy of the whole evaluation (init included), as the harness's
-    // elapsed covers the whole process (proj/src/harness.cpp:311-323)
+    // energy of the whole evaluation process: since the mark at the top of
+    // main (CUDA start-up included), as the harness's elapsed covers the
+    // whole process (proj/src/harness.cpp:311-323); without a mark, since the lease
     std::vector<uint64_t> e0(want, 0);
     bool energy_ok = true;
-    for (int i = 0; i < want; ++i) energy_ok = energy_ok && omcg_energy_counter_mj(gpus[i], &e0[i]) == OMCG_OK;
+    if (!marked)
+        for (int i = 0; i < want; ++i) energy_ok = energy_ok && omcg_energy_counter_mj(gpus[i], &e0[i]) == OMCG_OK;
     auto t0 = std::chrono::steady_clock::now();
     omcg_problem* p = nullptr;
     if (omcg_problem_create(kind, xs_seed, cfg.host_threads, &p) != OMCG_OK) {
@@ -193,11 +229,18 @@ int main(int argc, char** argv) {
     std::printf("FOM: %.6e particles/s\n", res.fom);
     std::fflush(stdout);
     omcg_problem_free(p);
+    omcg_release_devices();  // device teardown inside the metered span, not in the exit after it
     double joules = 0.0;
     for (int i = 0; i < want && energy_ok; ++i) {
-        uint64_t e1 = 0;
-        energy_ok = omcg_energy_counter_mj(gpus[i], &e1) == OMCG_OK;
-        joules += (double)(e1 - e0[i]) * 1e-3;
+        if (marked) {
+            double j = 0.0;
+            energy_ok = omcg_energy_since_mark_j(gpus[i], &j) == OMCG_OK;
+            joules += j;
+        } else {
+            uint64_t e1 = 0;
+            energy_ok = omcg_energy_counter_mj(gpus[i], &e1) == OMCG_OK;
+            joules += (double)(e1 - e0[i]) * 1e-3;
+        }
     }
     if (!energy_ok) joules = res.energy_j;  // NVML gone mid-run: the transport call's own reading
     // GPU energy in the package field; DRAM energy is not metered separately (HBM is inside the GPU's reading)
@@ -205,8 +248,11 @@ int main(int argc, char** argv) {
         std::fprintf(f, "%.6f %.6f\n", joules, 0.0);
         std::fclose(f);
     }
-    std::fprintf(stderr, "energy %.1f J over %.3f s (GPU, whole evaluation after the lease)\n", joules,
-                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    const auto t_end = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "energy %.1f J over %.3f s (GPU, %s) ; lease to exit %.3f s ; exec to main %.2f s\n",
+                 joules, std::chrono::duration<double>(t_end - (marked ? t_proc : t0)).count(),
+                 marked ? "whole process" : "from the lease", std::chrono::duration<double>(t_end - t0).count(),
+                 pre_main);
     for (int fd : fds) ::close(fd);
     return 0;
 }

@@ -90,9 +90,11 @@ thread_local std::vector<int64_t> t_trace;
 // a later run in the same process (the in-process evaluator, bench passes)
 // reuses them. Allocated on the legacy stream and synchronised at once, so
 // any stream may use the memory.
+std::mutex g_pool_mu;
+bool g_pool_done[64] = {};  // devices whose pool threshold is raised (= devices this process used)
 void keep_pool_memory(int device) {
-    static std::mutex mu;
-    static bool done[64] = {};
+    std::mutex& mu = g_pool_mu;
+    bool* done = g_pool_done;
     std::lock_guard<std::mutex> lk(mu);
     if (device < 0 || device >= 64 || done[device]) return;
     cudaMemPool_t pool;
@@ -124,6 +126,11 @@ struct PinnedSlab {
         if (!p) return;
         std::lock_guard<std::mutex> lk(mu);
         free_blocks.push_back(p);
+    }
+    void release() {  // (no run in flight) free every block
+        std::lock_guard<std::mutex> lk(mu);
+        for (void* p : free_blocks) cudaFreeHost(p);
+        free_blocks.clear();
     }
 };
 PinnedSlab& pinned() {
@@ -1156,12 +1163,16 @@ typedef int (*nvml_init_t)(void);
 typedef int (*nvml_by_pci_t)(const char*, void**);
 typedef int (*nvml_energy_t)(void*, unsigned long long*);
 typedef int (*nvml_power_t)(void*, unsigned int*);
+typedef int (*nvml_count_t)(unsigned int*);
+typedef int (*nvml_by_index_t)(unsigned int, void**);
 struct Nvml {
     void* lib = nullptr;
     nvml_init_t init = nullptr;
     nvml_by_pci_t by_pci = nullptr;
     nvml_energy_t energy = nullptr;
     nvml_power_t power = nullptr;  // optional: mW, for runs shorter than the energy counter's update period
+    nvml_count_t count = nullptr;
+    nvml_by_index_t by_index = nullptr;
     bool ok = false;
     Nvml() {
         lib = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
@@ -1170,6 +1181,8 @@ struct Nvml {
         by_pci = (nvml_by_pci_t)dlsym(lib, "nvmlDeviceGetHandleByPciBusId_v2");
         energy = (nvml_energy_t)dlsym(lib, "nvmlDeviceGetTotalEnergyConsumption");
         power = (nvml_power_t)dlsym(lib, "nvmlDeviceGetPowerUsage");
+        count = (nvml_count_t)dlsym(lib, "nvmlDeviceGetCount_v2");
+        by_index = (nvml_by_index_t)dlsym(lib, "nvmlDeviceGetHandleByIndex_v2");
         ok = init && by_pci && energy && init() == 0;
     }
 };
@@ -1189,6 +1202,77 @@ bool energy_counter_mj(int cuda_device, unsigned long long* mj) {
     }
     void* h = nullptr;
     return N.by_pci(bus, &h) == 0 && N.energy(h, mj) == 0;
+}
+
+// Process-start energy marks: every NVML device's counter, read through NVML
+// alone (no CUDA initialisation), matched to CUDA devices later by handle
+// (NVML returns one handle per physical device, by index or by PCI bus id).
+namespace {
+std::mutex g_mark_mu;
+std::vector<std::pair<void*, unsigned long long>> g_marks;
+}  // namespace
+
+// End of a process's GPU work (bin/openmc, before its last energy reading):
+// return the pooled device memory and the pinned words, and destroy the
+// device contexts, so that this teardown -- seconds' worth of unmapping at
+// P1 = 8e6 -- happens inside the metered span instead of in the process
+// exit after it. No omcg call may be in flight; later calls start afresh.
+void release_devices() {
+    {   // cached communicators live in the contexts about to be destroyed
+        CommCache& cc = comm_cache();
+        std::lock_guard<std::mutex> lk(cc.mu);
+        for (auto& e : cc.entries)
+            for (ncclComm_t cm : e->comms)
+                if (cm) ncclCommDestroy(cm);
+        cc.entries.clear();
+    }
+    pinned().release();
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (int d = 0; d < 64; ++d) {
+        if (!g_pool_done[d]) continue;
+        if (cudaSetDevice(d) == cudaSuccess) {
+            cudaDeviceSynchronize();
+            cudaDeviceReset();
+        }
+        g_pool_done[d] = false;
+    }
+    cudaGetLastError();
+}
+
+bool energy_mark() {
+    Nvml& N = nvml();
+    if (!N.ok || !N.count || !N.by_index) return false;
+    unsigned int n = 0;
+    if (N.count(&n) != 0) return false;
+    std::vector<std::pair<void*, unsigned long long>> marks;
+    for (unsigned int i = 0; i < n; ++i) {
+        void* h = nullptr;
+        unsigned long long mj = 0;
+        if (N.by_index(i, &h) == 0 && N.energy(h, &mj) == 0) marks.emplace_back(h, mj);
+    }
+    std::lock_guard<std::mutex> lk(g_mark_mu);
+    g_marks = std::move(marks);
+    return !g_marks.empty();
+}
+
+bool energy_since_mark_j(int cuda_device, double* joules) {
+    Nvml& N = nvml();
+    if (!N.ok) return false;
+    char bus[64];
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, cuda_device) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    void* h = nullptr;
+    unsigned long long mj = 0;
+    if (N.by_pci(bus, &h) != 0 || N.energy(h, &mj) != 0) return false;
+    std::lock_guard<std::mutex> lk(g_mark_mu);
+    for (const auto& m : g_marks)
+        if (m.first == h) {
+            *joules = (double)(mj - m.second) * 1e-3;
+            return true;
+        }
+    return false;
 }
 
 bool EnergyMeter::start(const std::vector<int>& cuda_devices) {

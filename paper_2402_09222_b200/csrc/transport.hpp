@@ -35,6 +35,11 @@ int device_count();
 
 // NVML cumulative energy of one CUDA device, mJ (false when unavailable)
 bool energy_counter_mj(int cuda_device, unsigned long long* mj);
+// process-start marks of every NVML device (no CUDA init), and the energy of
+// one CUDA device since them, J (false when unavailable / not marked)
+bool energy_mark();
+void release_devices();  // return pooled memory and destroy the contexts (no call in flight)
+bool energy_since_mark_j(int cuda_device, double* joules);
 
 // NVML energy counter (dlopen'ed; returns false when unavailable)
 struct EnergyMeter {

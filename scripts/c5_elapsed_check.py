@@ -1,18 +1,28 @@
 """EDP methodology check of a C5 campaign directory: per evaluation, the
 harness's elapsed (results.csv, proj/src/harness.cpp:311-323: EDP = energy x
-elapsed) against the binary's own wall time from its GPU lease to exit and the
-energy it wrote to metrics.txt over that same span (bin/openmc stderr line
-"energy <J> J over <s> s"). With workers <= leasable GPUs the two times agree
-to within process start-up (CUDA initialisation before the lease).
+elapsed) against the binary's own wall time over its whole process (main()
+entry to exit) and the energy it wrote to metrics.txt over that same span
+(bin/openmc stderr line "energy <J> J over <s> s (GPU, whole process)"; the
+NVML marks are taken before CUDA is initialised). With workers <= leasable
+GPUs no evaluation waits for another's lease, so the two times agree to
+within process creation (exec, dynamic loading) and the harness's polling.
 
-usage: python scripts/c5_elapsed_check.py <campaign out dir>
+It then re-runs the first --standalone K evaluations (default 6) standalone
+the way the harness spawns them (/bin/sh script <launcher args> in the
+evaluation's directory, AUTOTUNE_LAUNCHER_ARGS set), timed from outside on
+the wall clock, and compares the harness's elapsed with that standalone time
+(the "elapsed equals the standalone run time" criterion).
+
+usage: python scripts/c5_elapsed_check.py <campaign out dir> [--standalone K]
 """
 import csv
 import json
 import os
 import re
 import statistics
+import subprocess
 import sys
+import time
 
 out = sys.argv[1]
 rows = list(csv.DictReader(open(os.path.join(out, "results.csv"))))
@@ -37,4 +47,25 @@ summary = {
         abs(p["objective_edp"] - p["energy_j"] * p["harness_elapsed_s"]) <= 1e-3 * max(1.0, p["objective_edp"])
         for p in pts),
 }
-print(json.dumps({"summary": summary, "points": pts[:10]}, indent=1))
+K = int(sys.argv[sys.argv.index("--standalone") + 1]) if "--standalone" in sys.argv else 6
+standalone = []
+for p in pts[:K]:
+    d = os.path.join(out, "evals", str(p["eval_id"]))
+    la = open(os.path.join(d, "launcher")).read().strip() if os.path.exists(os.path.join(d, "launcher")) else ""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, AUTOTUNE_LAUNCHER_ARGS=la, PATH=os.path.join(root, "bin") + ":" + os.environ["PATH"])
+    for k, v in (("OMCG_PROBLEM", "assembly"), ("OMCG_PARTICLES", "1000000"), ("OMCG_BATCHES", "6"),
+                 ("OMCG_INACTIVE", "2")):  # scripts/run_campaign.sh's defaults
+        env.setdefault(k, v)
+    t0 = time.perf_counter()
+    r = subprocess.run(["/bin/sh", "script"] + la.split(), cwd=d, env=env, stdin=subprocess.DEVNULL,
+                       stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    wall = time.perf_counter() - t0
+    standalone.append({"eval_id": p["eval_id"], "rc": r.returncode, "standalone_wall_s": wall,
+                       "harness_elapsed_s": p["harness_elapsed_s"],
+                       "elapsed_over_standalone": p["harness_elapsed_s"] / wall})
+if standalone:
+    rs = [x["elapsed_over_standalone"] for x in standalone]
+    summary["elapsed_over_standalone_wall"] = {"median": statistics.median(rs), "min": min(rs), "max": max(rs),
+                                               "n": len(rs)}
+print(json.dumps({"summary": summary, "standalone": standalone, "points": pts[:10]}, indent=1))

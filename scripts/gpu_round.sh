@@ -1,5 +1,5 @@
-# Quick round check on the GPU box: GPU tests, smoke, bench line.
-set -x
-timeout 1500 python -m pytest tests/ -q -m gpu 2>&1 | tail -3
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+# Round pass on one B200: -m gpu suite + smoke, the bench line (3 runs), the
+# C5 EDP campaign (256 evaluations, 1 worker) and its elapsed-vs-run-time check.
+bash scripts/gpu_tests.sh
+for i in 1 2 3; do timeout 600 python bench.py > gpurun_out/bench_$i.json 2> gpurun_out/bench_$i.err; tail -1 gpurun_out/bench_$i.json | cut -c1-200; done
+bash scripts/gpu_c5_edp.sh

@@ -6,7 +6,7 @@ for tool in memcheck racecheck synccheck initcheck; do
   for c in pincell_queued pincell_queueless pincell_unfused pincell_cap1_p5 pincell_2rank pincell_nccl1 assembly_queued assembly_queueless assembly_unfused; do
     extra=""
     [ "$tool" = racecheck ] && extra="--racecheck-report analysis"
-    timeout 900 $S --tool $tool $extra --error-exitcode 9 --target-processes all python scripts/sanitize_case.py $c > gpurun_out/sanitize/${tool}_${c}.txt 2>&1
+    timeout 420 $S --tool $tool $extra --error-exitcode 9 --target-processes all python scripts/sanitize_case.py $c > gpurun_out/sanitize/${tool}_${c}.txt 2>&1
     rc=$?
     echo "$tool $c rc=$rc $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/sanitize/${tool}_${c}.txt | tr '\n' ' ') $(grep -E 'parity' gpurun_out/sanitize/${tool}_${c}.txt)" >> gpurun_out/sanitize/summary.txt
   done
