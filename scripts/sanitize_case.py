@@ -19,7 +19,7 @@ CASES = {
     "pincell_queued": ("pincell", 2000, dict(particles_in_flight=1000, tail_threshold=200, sort_threshold=0)),
     "pincell_queueless": ("pincell", 2000, dict(mode="openmc-queueless", particles_in_flight=1000, tail_threshold=100)),
     "pincell_unfused": ("pincell", 2000, dict(particles_in_flight=1000, event_fusion=0, tail_threshold=100)),
-    "pincell_cap1_p5": ("pincell", 2000, dict(particles_in_flight=700, move_event_cap=1, tasks_per_gpu=2)),
+    "pincell_cap1_p5": ("pincell", 600, dict(particles_in_flight=300, move_event_cap=1, tasks_per_gpu=2)),
     "pincell_2rank": ("pincell", 2000, dict(particles_in_flight=1000, n_gpus=2, devices=[0, 0])),
     "pincell_nccl1": ("pincell", 2000, dict(particles_in_flight=1000, force_nccl=True)),
     "assembly_queued": ("assembly", 600, dict(particles_in_flight=600, sort_threshold=100, tail_threshold=50)),
