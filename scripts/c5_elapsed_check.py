@@ -59,11 +59,23 @@ for p in pts[:K]:
         env.setdefault(k, v)
     t0 = time.perf_counter()
     r = subprocess.run(["/bin/sh", "script"] + la.split(), cwd=d, env=env, stdin=subprocess.DEVNULL,
-                       stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+                       capture_output=True, text=True)
     wall = time.perf_counter() - t0
+
+    def fom(txt):
+        m = re.findall(r"FOM:\s*([0-9.eE+-]+)", txt)
+        return float(m[-1]) if m else None
+
+    def line(txt, key):
+        return next((x.strip() for x in txt.splitlines() if key in x), None)
+
+    camp_out = open(os.path.join(d, "stdout.log")).read() if os.path.exists(os.path.join(d, "stdout.log")) else ""
+    camp_err = open(os.path.join(d, "stderr.log")).read() if os.path.exists(os.path.join(d, "stderr.log")) else ""
     standalone.append({"eval_id": p["eval_id"], "rc": r.returncode, "standalone_wall_s": wall,
                        "harness_elapsed_s": p["harness_elapsed_s"],
-                       "elapsed_over_standalone": p["harness_elapsed_s"] / wall})
+                       "elapsed_over_standalone": p["harness_elapsed_s"] / wall,
+                       "launcher": la, "fom_campaign": fom(camp_out), "fom_standalone": fom(r.stdout),
+                       "energy_line_campaign": line(camp_err, "energy "), "energy_line_standalone": line(r.stderr, "energy ")})
 if standalone:
     rs = [x["elapsed_over_standalone"] for x in standalone]
     summary["elapsed_over_standalone_wall"] = {"median": statistics.median(rs), "min": min(rs), "max": max(rs),
