@@ -75,7 +75,8 @@ for p in pts[:K]:
                        "harness_elapsed_s": p["harness_elapsed_s"],
                        "elapsed_over_standalone": p["harness_elapsed_s"] / wall,
                        "launcher": la, "fom_campaign": fom(camp_out), "fom_standalone": fom(r.stdout),
-                       "energy_line_campaign": line(camp_err, "energy "), "energy_line_standalone": line(r.stderr, "energy ")})
+                       "energy_line_campaign": line(camp_err, "energy "), "energy_line_standalone": line(r.stderr, "energy "),
+                       "stderr_standalone": r.stderr[-3000:] if os.environ.get("OMCG_TRACE_INIT") else None})
 if standalone:
     rs = [x["elapsed_over_standalone"] for x in standalone]
     summary["elapsed_over_standalone_wall"] = {"median": statistics.median(rs), "min": min(rs), "max": max(rs),
