@@ -238,6 +238,7 @@ def roof_fields(k, items, ms, peak):
     return {"dram_bytes_per_item": per, "dram_achieved_gbs": dram,
             "dram_frac": dram / peak if dram else None,
             "binding_roof": {"name": k.get("binding"), "l1tex_throughput_pct": k.get("l1tex_pct"),
+                             "l1_data_pipe_wavefronts_pct": k.get("l1_data_pipe_wavefronts_pct"),
                              "issue_active_pct": k.get("issue_active_pct"),
                              "lanes_per_instruction": k.get("lanes_per_inst"),
                              "warps_per_sm": k.get("warps_per_sm"), "l2_hit_pct": k.get("l2_hit_pct"),

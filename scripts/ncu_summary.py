@@ -25,6 +25,9 @@ METRICS = [
     "smsp__thread_inst_executed_per_inst_executed.ratio", "smsp__inst_executed.sum",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__lsu_writeback_active.avg.pct_of_peak_sustained_elapsed",
+    "smsp__inst_executed_op_shfl.sum",
 ]
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "us": 1e-6, "usecond": 1e-6,
               "ms": 1e-3, "msecond": 1e-3, "ns": 1e-9, "nsecond": 1e-9, "s": 1, "second": 1,
@@ -99,6 +102,7 @@ def main():
         issue = x.get("smsp__issue_active.avg.pct_of_peak_sustained_active")
         d = {"binding": "L1/TEX throughput" if (l1 or 0) >= (issue or 0) else "issue (latency-bound warps)",
              "l1tex_pct": l1, "issue_active_pct": issue,
+             "l1_data_pipe_wavefronts_pct": x.get("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
              "lanes_per_inst": x.get("smsp__thread_inst_executed_per_inst_executed.ratio"),
              "warps_per_sm": x.get("sm__warps_active.avg.per_cycle_active"),
              "l2_hit_pct": x.get("lts__t_sector_hit_rate.pct"),
