@@ -32,6 +32,8 @@ struct DevLib {
     const uint8_t* mat_fissionable;
     const uint8_t* mat_fuel;  // material uses the fuel XS queue
     const uint8_t* mat_sort_rank;  // fuel material rank for the sort key
+    const double* host_dens;       // host copy of mat_dens (launch parameters), nullptr if too large
+    int n_dens;                    // entries in host_dens
 };
 
 struct Site {

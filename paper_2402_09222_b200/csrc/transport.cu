@@ -167,6 +167,7 @@ struct GpuProblem {
     Geometry geo{};
     int n_fuel_mats = 0;
     int max_fuel_seg = 1;  // 16-nuclide segments of the largest fuel-queue material
+    std::vector<double> host_dens;  // lib.host_dens points here (lifetime of the upload)
     int64_t h2d_bytes = 0;
 
     void upload(const Problem& p, int n_bins, int device, cudaStream_t s) {
@@ -258,6 +259,9 @@ struct GpuProblem {
         lib.goff = d_goff; lib.E = d_E; lib.xs = d_xs; lib.hash = d_hash; lib.awr = d_awr;
         lib.mat_off = d_moff; lib.mat_nuc = d_mnuc; lib.mat_desc = d_mdesc; lib.mat_dens = d_mdens;
         lib.mat_fissionable = d_mfis; lib.mat_fuel = d_mfuel; lib.mat_sort_rank = d_mrank;
+        host_dens = mdens;  // launch-parameter copy of the densities (fuel lookup)
+        lib.host_dens = host_dens.data();
+        lib.n_dens = (int)host_dens.size();
         launch_hash_build(lib, d_hash, s);
         CK(cudaGetLastError());
         geo = p.geo;
