@@ -47,3 +47,20 @@ def test_clock_sampler_degrades_without_a_gpu():
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d, k
     assert isinstance(d["reasons"], list)
+
+
+def test_roofline_fields_from_committed_ncu():
+    """bench.py's roofline extras come from the committed ncu summary: the fuel
+    lookup's DRAM rate is a true HBM fraction (well below 1, unlike the
+    algorithmic-byte `frac`), and the binding roof is the L1 data pipe."""
+    sys.path.insert(0, ROOT)
+    import bench
+    roofs = bench.ncu_roofs()
+    k = roofs["k_xs_fuel_fused"]
+    f = bench.roof_fields(k, 1e6, 1.3, 6554.9)
+    assert 0.0 < f["dram_frac"] < 0.2
+    br = f["binding_roof"]
+    assert br["name"] == "L1/TEX throughput"
+    assert br["l1_data_pipe_wavefronts_pct"] > 50.0
+    assert br["source"].startswith("profiles/")
+    assert os.path.exists(os.path.join(ROOT, br["source"].split(" ")[0]))
