@@ -92,6 +92,8 @@ void launch_collide(const Ctx& c, const int32_t* q, int n, int n_front, cudaStre
 void launch_move(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
 // diagnostic build only (-DOMCG_MOVE_CYCLES): per-event-type cycle shares of k_move to stderr
 void dump_move_cycles();
+// diagnostic build only (-DOMCG_COOP_STATS): fuel-lookup blocks on the cooperative / per-lane path
+void dump_coop_stats();
 // diagnostic build only (-DOMCG_TAIL_CYCLES): per-event-type cycles of the tail's longest history to stderr
 void dump_tail_cycles();
 

@@ -1398,6 +1398,7 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
     }
     mark("ranks done");
     if (std::getenv("OMCG_MOVE_CYCLES")) dump_move_cycles();
+    if (std::getenv("OMCG_COOP_STATS")) dump_coop_stats();
     if (std::getenv("OMCG_TAIL_CYCLES")) dump_tail_cycles();
     std::exception_ptr first;
     for (auto& e : errs)
