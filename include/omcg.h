@@ -121,6 +121,13 @@ typedef struct {
      * different GPUs. Communicators are created once per placement and reused
      * by later calls in the same process. */
     int force_nccl;
+    /* Queued mode with event fusion, once the source is exhausted: 1 (default)
+     * lets the GPU apply the longest-queue rule itself — the kernel that ends
+     * an iteration records the next choice, and the host enqueues candidate
+     * kernels ahead without reading queue lengths back (a candidate that is
+     * not the recorded choice returns at once). 0: the host reads the
+     * lengths back and picks every iteration. Same iterations, same results. */
+    int device_schedule;
 } omcg_run_config;
 
 typedef struct {

@@ -122,7 +122,7 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
                 n_batches=15, n_inactive=5, seed=1, n_gpus=1, devices=None, world_size=1, rank=0,
                 nccl_id: bytes | None = None, record_batch=0, record_n=0, profile=False,
                 trace_queues=False, tail_threshold=None, event_fusion=None, move_event_cap=None,
-                force_nccl=False) -> RunConfig:
+                force_nccl=False, device_schedule=None) -> RunConfig:
     cfg = RunConfig()
     _lib.omcg_run_config_default(C.byref(cfg))
     m = {"openmc": QUEUED, "queued": QUEUED, "openmc-queueless": QUEUELESS,
@@ -159,6 +159,8 @@ def make_config(mode="openmc", particles_in_flight=1_000_000, n_bins=4000, sort_
     if move_event_cap is not None:
         cfg.move_event_cap = int(move_event_cap)
     cfg.force_nccl = int(bool(force_nccl))
+    if device_schedule is not None:
+        cfg.device_schedule = int(device_schedule)
     return cfg
 
 

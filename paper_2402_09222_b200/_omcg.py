@@ -48,6 +48,7 @@ class RunConfig(C.Structure):
         ("nccl_id", C.c_ubyte * 128), ("record_batch", C.c_int), ("record_n", C.c_int64),
         ("profile", C.c_int), ("trace_queues", C.c_int), ("tail_threshold", C.c_int64),
         ("event_fusion", C.c_int), ("move_event_cap", C.c_int), ("force_nccl", C.c_int),
+        ("device_schedule", C.c_int),
     ]
 
 

@@ -122,6 +122,9 @@ OMCG_API int omcg_xs_lookup_queue(const omcg_problem* p, int n_bins, int device,
         omcg::device_xs_lookup_queue(p->p, n_bins, device, n, mat, E, sort_threshold, out, ckpt_out);
     });
 }
+#ifndef OMCG_DEFAULT_DEVICE_SCHEDULE
+#define OMCG_DEFAULT_DEVICE_SCHEDULE 0
+#endif
 OMCG_API void omcg_run_config_default(omcg_run_config* c) {
     if (!c) return;
     std::memset(c, 0, sizeof *c);
@@ -145,6 +148,7 @@ OMCG_API void omcg_run_config_default(omcg_run_config* c) {
     c->tail_threshold = 16384;
     c->event_fusion = 1;
     c->move_event_cap = 20;
+    c->device_schedule = OMCG_DEFAULT_DEVICE_SCHEDULE;
 }
 
 OMCG_API int omcg_run(const omcg_problem* p, const omcg_run_config* cfg, omcg_run_result* res, int64_t* tally_out,

@@ -20,6 +20,27 @@ struct QueueSet {
 };
 constexpr int ADV_ALT = 6;  // the second move-queue region (N_QUEUES + 1 regions are allocated)
 
+// Device-driven queued loop (omcg_run_config.device_schedule): the kernel that
+// completes an iteration applies the longest-queue rule itself (its last
+// block, after every append) and writes the next iteration's choice here; the
+// host enqueues candidate kernels ahead without reading counts back, and each
+// candidate returns at once unless it is the recorded choice.
+constexpr int SCHED_TAIL = 6;  // choice: few enough histories left for the tail kernel
+constexpr int SCHED_DONE = 7;  // choice: every history of the sub-bank has finished
+struct DevSched {
+    int choice;      // EV_XS_FUEL / EV_ADV / EV_COLL, or SCHED_TAIL / SCHED_DONE
+    int n;           // length of the chosen queue
+    int n_front;     // collision queue: fuel entries at the front
+    int sorted;      // fuel lookup: the queue is sorted first (n >= P3)
+    int drain_q;     // move: region being drained
+    int app_q;       // region receiving move-queue appends during this iteration
+    int executed;    // iterations completed since the host handed over
+    int cur;         // index of the current iteration (trace log)
+    int sorts;       // sorted fuel lookups
+    unsigned ticket; // last-block ticket of the running kernel
+    unsigned long long chunk;  // work counter of the persistent fuel lookup
+};
+
 // Everything an event kernel needs, passed by value as the kernel parameter.
 struct Ctx {
     QueueSet qs;
@@ -43,6 +64,13 @@ struct Ctx {
     unsigned long long* ctrl;  // [0] refill ticket, [1] alive, [2] error flags, [3] tail list, [4] move chunks, [5] queueless lookup chunks
     int fused;                 // event fusion: non-fuel XS work goes to the move (advance) queue
     int move_cap;              // > 0: a history runs at most move_cap events per move launch, then rejoins the move queue
+    // device-driven loop (nullptr: the host picks every iteration)
+    DevSched* sched;
+    int* sched_log;            // per iteration {choice, n} (max_iters entries)
+    unsigned long long* sched_chk;  // trace mode: per-iteration id checksums
+    int sched_max_iters;
+    int sort_threshold;        // P3 (-1: never)
+    int64_t tail_threshold;
 };
 
 constexpr int SMEM_TALLY_MAX = 64;  // tally bins*scores aggregated per block in smem (few-pin problems)
@@ -90,6 +118,14 @@ void launch_collide(const Ctx& c, const int32_t* q, int n, int n_front, cudaStre
 // (the queueless sweep, q == nullptr, runs the non-fuel collisions inside the
 // loop too)
 void launch_move(const Ctx& c, const int32_t* q, int n, cudaStream_t s);
+
+// device-driven loop candidates (Ctx::sched set): each returns at once unless
+// the recorded choice is its event; lengths come from the device
+void launch_fuel_candidate(const Ctx& c, const int32_t* q_fuel, int32_t* q_sorted, int nseg, int n_fuel_mats,
+                           unsigned int* hist, unsigned int* cursor, uint32_t* keys, unsigned int* bsum,
+                           cudaStream_t s);
+void launch_move_candidate(const Ctx& c, cudaStream_t s);
+void launch_collide_candidate(const Ctx& c, cudaStream_t s);
 // diagnostic build only (-DOMCG_MOVE_CYCLES): per-event-type cycle shares of k_move to stderr
 void dump_move_cycles();
 // diagnostic build only (-DOMCG_COOP_STATS): fuel-lookup blocks on the cooperative / per-lane path

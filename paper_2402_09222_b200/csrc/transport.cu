@@ -269,6 +269,9 @@ struct GpuProblem {
     }
 };
 
+constexpr int SCHED_RING = 8;       // read-backs of the schedule record in flight
+constexpr int SCHED_LOG = 1 << 16;  // iterations per device-driven stretch
+
 struct SubBank {
     cudaStream_t stream = nullptr;
     Bank b{};
@@ -302,6 +305,13 @@ struct SubBank {
     int64_t prof_items[8] = {};
     double xs_fuel_bytes = 0.0;
     int64_t iterations = 0, sorts = 0;
+    // device-driven queued loop: schedule record, per-iteration log and
+    // checksums, pinned read-back ring
+    DevSched* sched = nullptr;
+    int* sched_log = nullptr;
+    ull* sched_chk = nullptr;
+    DevSched* h_sched[SCHED_RING + 1] = {};
+    cudaEvent_t sched_ev[SCHED_RING] = {};
 };
 
 struct BatchComm;
@@ -451,6 +461,12 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         S.h_counts = static_cast<unsigned*>(pinned().get());  // 8 words
         S.h_ctrl = static_cast<ull*>(pinned().get());         // 4 words
         S.h_trace_chk = static_cast<ull*>(pinned().get());
+        S.sched = A.alloc<DevSched>(1);
+        S.sched_log = A.alloc<int>(2 * (int64_t)SCHED_LOG);
+        S.sched_chk = A.alloc<ull>(SCHED_LOG);
+        static_assert(sizeof(DevSched) <= 64, "schedule record must fit a pinned block");
+        for (auto& h : S.h_sched) h = static_cast<DevSched*>(pinned().get());
+        for (auto& e : S.sched_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         S.evs.resize(64);
         for (auto& e : S.evs) {
             CK(cudaEventCreate(&e.a));
@@ -478,6 +494,9 @@ void teardown_rank(Rank& R) {
         pinned().put(S.h_counts);
         pinned().put(S.h_ctrl);
         pinned().put(S.h_trace_chk);
+        for (auto& h : S.h_sched) pinned().put(h);
+        for (auto& e : S.sched_ev)
+            if (e) cudaEventDestroy(e);
         mark("host buffers");
         for (auto& e : S.evs) {
             if (e.a) cudaEventDestroy(e.a);
@@ -535,6 +554,112 @@ struct Prof {
     }
 };
 
+// Device-driven stretch of the queued loop (cfg.device_schedule, event fusion,
+// source exhausted): the host hands the current choice to the GPU, then keeps
+// enqueueing candidates in the usual order of a history's cycle (fuel lookup,
+// move, collision, move) without waiting; the kernel that ends an iteration
+// records the next choice (the same longest-queue rule), candidates that are
+// not the recorded choice return at once. The schedule record is read back
+// asynchronously; the stretch ends when the GPU records "tail" or "done".
+// Returns with the stream synchronised and c.qs.adv_q updated.
+void run_device_loop(Rank& R, SubBank& S, Ctx& c, const omcg_run_config& cfg, bool prof, int fuel_nuc, int best,
+                     int n, const int64_t* qlen) {
+    const bool trace = cfg.trace_queues != 0;
+    DevSched& h = *S.h_sched[SCHED_RING];
+    h = DevSched{};
+    h.choice = best;
+    h.n = n;
+    h.n_front = (int)S.h_counts[EV_COLL];
+    h.sorted = best == EV_XS_FUEL && cfg.sort_threshold >= 0 && qlen[best] >= cfg.sort_threshold ? 1 : 0;
+    h.sorts = h.sorted;
+    h.app_q = h.drain_q = c.qs.adv_q;
+    if (best == EV_ADV && c.move_cap) h.app_q = c.qs.adv_q == EV_ADV ? ADV_ALT : EV_ADV;
+    CK(cudaMemcpyAsync(S.sched, &h, sizeof(DevSched), cudaMemcpyHostToDevice, S.stream));
+    if (trace) CK(cudaMemsetAsync(S.sched_chk, 0, sizeof(ull) * SCHED_LOG, S.stream));
+    Ctx cs = c;
+    cs.sched = S.sched;
+    cs.sched_log = S.sched_log;
+    cs.sched_chk = trace ? S.sched_chk : nullptr;
+    cs.sched_max_iters = SCHED_LOG;
+    cs.sort_threshold = cfg.sort_threshold >= 0 && cfg.sort_threshold < (1LL << 31) ? (int)cfg.sort_threshold
+                        : cfg.sort_threshold < 0 ? -1 : 0x7fffffff;
+    cs.tail_threshold = cfg.tail_threshold;
+    cs.trace_chk = nullptr;
+    const int32_t* q_fuel = S.qs.qbase + (int64_t)EV_XS_FUEL * S.qs.cap;
+    static const int pattern[4] = {EV_XS_FUEL, EV_ADV, EV_COLL, EV_ADV};
+    int pos = best == EV_XS_FUEL ? 0 : best == EV_ADV ? 1 : 2;
+    int64_t w = 0, r = 0, last_exec = -1, stale = 0;
+    bool stop = false;
+    while (!stop) {
+        for (int j = 0; j < 4; ++j, ++pos) {
+            const int k = pattern[pos & 3];
+            Prof pf(S, prof, k == EV_XS_FUEL ? 0 : k == EV_ADV ? 2 : 4, 0);
+            if (k == EV_XS_FUEL)
+                launch_fuel_candidate(cs, q_fuel, S.q_sorted, R.gp.max_fuel_seg, R.gp.n_fuel_mats, S.hist, S.cursor,
+                                      S.keys, S.bsum, S.stream);
+            else if (k == EV_ADV)
+                launch_move_candidate(cs, S.stream);
+            else
+                launch_collide_candidate(cs, S.stream);
+        }
+        const int slot = (int)(w % SCHED_RING);
+        CK(cudaMemcpyAsync(S.h_sched[slot], S.sched, sizeof(DevSched), cudaMemcpyDeviceToHost, S.stream));
+        CK(cudaEventRecord(S.sched_ev[slot], S.stream));
+        ++w;
+        while (r < w) {  // look at the read-backs that have landed (wait only when the ring is full)
+            const int rs = (int)(r % SCHED_RING);
+            if (w - r >= SCHED_RING) CK(cudaEventSynchronize(S.sched_ev[rs]));
+            else if (cudaEventQuery(S.sched_ev[rs]) != cudaSuccess) {
+                cudaGetLastError();
+                break;
+            }
+            const DevSched& x = *S.h_sched[rs];
+            ++r;
+            if (x.choice < SCHED_TAIL && (x.n < 0 || x.n > S.qs.cap))
+                throw std::logic_error("device-driven queue loop: queue " + std::to_string(x.choice) + " length " +
+                                       std::to_string(x.n) + " at iteration " + std::to_string(x.executed));
+            if (x.choice >= SCHED_TAIL) {
+                stop = true;
+                break;
+            }
+            if (x.executed == last_exec) {
+                if (++stale > 64) throw CudaError("device-driven queue loop made no progress");
+            } else {
+                stale = 0;
+                last_exec = x.executed;
+            }
+        }
+    }
+    CK(cudaStreamSynchronize(S.stream));
+    DevSched fin;
+    CK(cudaMemcpy(&fin, S.sched, sizeof(DevSched), cudaMemcpyDeviceToHost));
+    if (fin.choice < SCHED_TAIL) throw CudaError("device-driven queue loop stopped early");
+    if (prof) drain_profile(S);
+    S.iterations += fin.executed;
+    S.sorts += fin.sorts;
+    c.qs.adv_q = fin.app_q;
+    // the iterations' (queue, length): the host's own first entry, the rest from the device log
+    std::vector<int> log(2 * (size_t)std::max(fin.executed, 1));
+    if (fin.executed > 1)
+        CK(cudaMemcpy(log.data() + 2, S.sched_log + 2, sizeof(int) * 2 * (size_t)(fin.executed - 1),
+                      cudaMemcpyDeviceToHost));
+    log[0] = best;
+    log[1] = n;
+    if (prof)
+        for (int i = 0; i < fin.executed; ++i)
+            if (log[2 * i] == EV_XS_FUEL) S.xs_fuel_bytes += (double)log[2 * i + 1] * (44.0 + 100.0 * (double)fuel_nuc);
+    if (trace) {
+        std::vector<ull> chk((size_t)fin.executed);
+        if (fin.executed > 0)
+            CK(cudaMemcpy(chk.data(), S.sched_chk, sizeof(ull) * (size_t)fin.executed, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < fin.executed; ++i) {
+            S.trace.push_back(log[2 * i]);
+            S.trace.push_back(log[2 * i + 1]);
+            S.trace.push_back((int64_t)chk[(size_t)i]);
+        }
+    }
+}
+
 void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_config& cfg, bool prof,
                 int fuel_nuc) {
     int64_t next = S.lo;
@@ -583,6 +708,14 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
             for (int k = 1; k < EV_DEAD; ++k)
                 if (qlen[k] > qlen[best]) best = k;
             int n = (int)qlen[best];
+            if (cfg.device_schedule && c.fused && next >= S.hi && live > tail &&
+                (best == EV_XS_FUEL || best == EV_ADV || best == EV_COLL)) {
+                S.iterations--;  // counted by the device-driven stretch
+                c.trace_chk = nullptr;
+                run_device_loop(R, S, c, cfg, prof, fuel_nuc, best, n, qlen);
+                known = false;
+                continue;
+            }
             if (next >= S.hi && live <= tail) {
                 // sparse end of the batch: one launch finishes every live history
                 best = EV_DEAD;

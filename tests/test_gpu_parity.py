@@ -116,24 +116,26 @@ def test_assembly_transport_bit_exact(fusion):
     _compare_runs(P.ASSEMBLY, 4000, 3, 1, 1000, particles_in_flight=4000, tail_threshold=100, event_fusion=fusion)
 
 
-@pytest.mark.parametrize("fusion,cap", [(1, 20), (1, 0), (1, 3), (0, 20)])
+@pytest.mark.parametrize("fusion,cap,dsched", [(1, 20, 0), (1, 0, 0), (1, 3, 0), (0, 20, 0), (1, 20, 1), (1, 0, 1),
+                                               (1, 3, 1)])
 @pytest.mark.parametrize("kind,n,in_flight,tail,sort", [
     (P.PINCELL, 6000, 1500, 300, 0),       # refill active, sorted fuel queue, tail
     (P.PINCELL, 4000, 4000, 0, -1),        # all in flight, no tail
     (P.ASSEMBLY, 3000, 1000, 200, 500),
 ])
-def test_queue_contents_bit_exact(kind, n, in_flight, tail, sort, fusion, cap):
+def test_queue_contents_bit_exact(kind, n, in_flight, tail, sort, fusion, cap, dsched):
     """North star: queue contents match. Per queued-mode iteration, the chosen
     queue, its length and the order-free checksum of its history ids equal the
     oracle's emulation of the same scheduling policy (batch 1), with and
-    without event fusion (the move kernel), and with the move kernel's
-    per-launch event cap at its default, off, and small."""
+    without event fusion (the move kernel), with the move kernel's
+    per-launch event cap at its default, off, and small, and with the queue
+    choice made on the host or by the GPU itself (device_schedule)."""
     o = O.Problem(kind, 1234, 4000)
     want = o.queue_trace(n, in_flight, tail, seed=1, event_fusion=bool(fusion), move_cap=cap)
     p = P.Problem(kind, 1234)
     out = P.run(p, n_particles=n, n_batches=1, n_inactive=0, seed=1, particles_in_flight=in_flight,
                 tail_threshold=tail, sort_threshold=sort, trace_queues=True, event_fusion=fusion,
-                move_event_cap=cap)
+                move_event_cap=cap, device_schedule=dsched)
     got = out.queue_trace
     assert got.shape == want.shape
     assert np.array_equal(got, want)
@@ -179,11 +181,15 @@ TUNED_VARIANTS = [
     dict(particles_in_flight=50000),
     # the per-batch exchanges through a one-rank NCCL communicator
     dict(particles_in_flight=5000, force_nccl=True),
+    # the queue choice made by the GPU itself (device-driven loop), with refill first and all in flight
+    dict(particles_in_flight=2000, device_schedule=1),
+    dict(particles_in_flight=10000, tail_threshold=0, device_schedule=1),
 ]
 ASSEMBLY_VARIANTS = TUNED_VARIANTS + [
     dict(particles_in_flight=10000, sort_threshold=500),  # the sort fires on the depleted fuel queue
     dict(particles_in_flight=2500, sort_threshold=500, tail_threshold=100),
     dict(mode="openmc-queueless", particles_in_flight=10000, tasks_per_gpu=2),
+    dict(particles_in_flight=10000, sort_threshold=500, device_schedule=1, tasks_per_gpu=2),
 ]
 
 
