@@ -154,6 +154,18 @@ def test_c2_bench_configuration_bit_exact():
     assert out.result.tail_launches == 3
 
 
+def test_c2_bench_configuration_device_schedule_bit_exact():
+    """The same bench configuration with the queue choice made on the GPU
+    (device-driven loop): identical results, and the same
+    number of queue iterations and sorts as the host-driven loop."""
+    n = 1_000_000
+    kw = dict(particles_in_flight=n, n_bins=4000, sort_threshold=20_000)
+    dev = _compare_runs(P.ASSEMBLY, n, 3, 1, 10_000, device_schedule=1, **kw)
+    host = P.run(P.Problem(P.ASSEMBLY, 1234), n_particles=n, n_batches=3, n_inactive=1, seed=1, **kw)
+    assert dev.result.queue_iterations == host.result.queue_iterations
+    assert dev.result.sorts == host.result.sorts
+
+
 TUNED_VARIANTS = [
     dict(particles_in_flight=1000),                       # P1 < N: dynamic refill
     dict(particles_in_flight=5000, sort_threshold=0),     # always sort
