@@ -3,7 +3,7 @@ synccheck / initcheck): python scripts/sanitize_case.py <case>. The run is also
 checked bit-for-bit against the oracle so a sanitizer pass is a correct pass.
 Cases cover the queued loop (event fusion, move cap, one kernel per event),
 queueless mode, the fuel-queue sort, the tail, P5 sub-banks, the 2-rank
-loopback exchange and the one-rank NCCL path."""
+loopback exchange, the one-rank NCCL path and the device-driven loop."""
 import os
 import sys
 
@@ -25,6 +25,11 @@ CASES = {
     "assembly_queued": ("assembly", 600, dict(particles_in_flight=600, sort_threshold=100, tail_threshold=50)),
     "assembly_queueless": ("assembly", 600, dict(mode="openmc-queueless", particles_in_flight=300, tail_threshold=50)),
     "assembly_unfused": ("assembly", 400, dict(particles_in_flight=400, event_fusion=0, tail_threshold=50)),
+    # the device-driven queued loop: guarded candidates, persistent fuel lookup and collisions
+    "pincell_dsq": ("pincell", 2000, dict(particles_in_flight=2000, tail_threshold=100, sort_threshold=0,
+                                          device_schedule=1)),
+    "assembly_dsq": ("assembly", 600, dict(particles_in_flight=600, sort_threshold=100, tail_threshold=50,
+                                           device_schedule=1)),
 }
 
 name = sys.argv[1]
