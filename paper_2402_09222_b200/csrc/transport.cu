@@ -836,6 +836,11 @@ struct BatchComm {
 
 // NCCL over NVLink between ranks on different GPUs.
 struct NcclBatchComm : BatchComm {
+    // self_p2p: a rank's own slice of the canonical bank also goes through
+    // ncclSend/ncclRecv (to itself) instead of a device copy, so a one-rank
+    // communicator (force_nccl) runs the point-to-point exchange on hardware
+    explicit NcclBatchComm(bool self_p2p = false) : self_p2p(self_p2p) {}
+    bool self_p2p;
     void reduce_batch(Rank& R, bool active) override {
         NK(ncclGroupStart());
         NK(ncclAllReduce(R.acc.k, R.acc.k, 3, ncclUint64, ncclSum, R.comm, R.main));
@@ -854,7 +859,7 @@ struct NcclBatchComm : BatchComm {
         NK(ncclGroupStart());
         for (int r = 0; r < W; ++r) {
             int64_t sf = plan[r], sc = plan[W + r], rf = plan[2 * W + r], rc = plan[3 * W + r];
-            if (r == R.rank) {
+            if (r == R.rank && !self_p2p) {
                 if (sc > 0)
                     CK(cudaMemcpyAsync(R.recv + rf, R.canon + sf, sizeof(Site) * (size_t)sc, cudaMemcpyDeviceToDevice,
                                        R.main));
@@ -1498,7 +1503,7 @@ void run_transport(const Problem& p, const omcg_run_config& cfg_in, omcg_run_res
         for (int i = 0; i < local_ranks; ++i) bcs[i].reset(new LoopbackBatchComm(loop_shared.get()));
     } else if (local_ranks > 1 || cfg.force_nccl) {
         lease.acquire_all(devs);
-        for (int i = 0; i < local_ranks; ++i) bcs[i].reset(new NcclBatchComm());
+        for (int i = 0; i < local_ranks; ++i) bcs[i].reset(new NcclBatchComm(local_ranks == 1));
     }
     mark("communicators");
     for (int i = 0; i < local_ranks; ++i) {
