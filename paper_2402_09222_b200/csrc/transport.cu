@@ -300,6 +300,7 @@ struct SubBank {
     };
     std::vector<EvPair> evs;  // deferred per-kernel timing, read after each host sync
     int n_pending = 0;
+    int n_done = 0;  // pending pairs known complete (recorded before the last host sync)
     double prof_ms[8] = {};
     int64_t prof_launches[8] = {};
     int64_t prof_items[8] = {};
@@ -532,6 +533,27 @@ void drain_profile(SubBank& S) {
         S.prof_items[S.evs[i].cls] += S.evs[i].items;
     }
     S.n_pending = 0;
+    S.n_done = 0;
+}
+
+// The pairs recorded before the last host sync are complete: read them while
+// the GPU runs the kernel just launched (no wait, off the host's critical
+// path between a read-back and the next launch), keep the newer ones.
+void drain_done(SubBank& S) {
+    const int k = S.n_done;
+    if (k == 0) return;
+    static const bool log = std::getenv("OMCG_PROF_LOG") != nullptr;
+    for (int i = 0; i < k; ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, S.evs[i].a, S.evs[i].b));
+        if (log) std::fprintf(stderr, "[launch] class %d items %lld ms %.4f\n", S.evs[i].cls, (long long)S.evs[i].items, ms);
+        S.prof_ms[S.evs[i].cls] += ms;
+        S.prof_launches[S.evs[i].cls] += 1;
+        S.prof_items[S.evs[i].cls] += S.evs[i].items;
+    }
+    std::rotate(S.evs.begin(), S.evs.begin() + k, S.evs.begin() + S.n_pending);
+    S.n_pending -= k;
+    S.n_done = 0;
 }
 
 struct Prof {
@@ -678,7 +700,7 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
             if (pending_trace)
                 CK(cudaMemcpyAsync(S.h_trace_chk, S.trace_chk, sizeof(ull), cudaMemcpyDeviceToHost, S.stream));
             CK(cudaStreamSynchronize(S.stream));
-            if (prof) drain_profile(S);
+            S.n_done = S.n_pending;  // read after the next launch (drain_done)
             if (check_prediction && std::memcmp(predicted, S.h_counts, sizeof predicted) != 0)
                 throw std::logic_error("queue-length prediction after a fuel calculate_xs launch was wrong");
             check_prediction = false;
@@ -782,7 +804,9 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
             S.dead_head += (uint64_t)n;
             next += n;
         }
+        if (prof) drain_done(S);
     }
+    if (prof) drain_profile(S);
 }
 
 void run_queueless(Rank& R, SubBank& S, Ctx c, const Site* src, bool prof, int64_t tail) {
