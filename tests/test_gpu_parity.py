@@ -225,6 +225,13 @@ def test_core_transport_bit_exact():
     assert out.result.n_leaked > 0
 
 
+def test_core_transport_at_scale_bit_exact():
+    """C4 at 2e5 histories per batch with the library defaults (sorted fuel
+    queue, warp-cooperative lookups, move cap, tail), 2 batches."""
+    out = _compare_runs(P.CORE, 200_000, 2, 1, 2000, particles_in_flight=200_000)
+    assert out.result.n_leaked > 0 and out.result.sorts > 0
+
+
 @pytest.mark.parametrize("kw", [
     dict(n_gpus=3, devices=[0, 0, 0], tasks_per_gpu=4),   # ragged: 7 histories over 12 sub-banks
     dict(particles_in_flight=2),
