@@ -3,7 +3,7 @@
 mkdir -p gpurun_out/sanitize
 S=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck racecheck synccheck initcheck; do
-  for c in pincell_queued pincell_queueless pincell_unfused pincell_cap1_p5 pincell_2rank pincell_nccl1 assembly_queued assembly_queueless assembly_unfused; do
+  for c in pincell_queued pincell_queueless pincell_unfused pincell_cap1_p5 pincell_2rank pincell_nccl1 assembly_queued assembly_queueless assembly_unfused pincell_dsq assembly_dsq; do
     extra=""
     [ "$tool" = racecheck ] && extra="--racecheck-report analysis"
     timeout 420 $S --tool $tool $extra --error-exitcode 9 --target-processes all python scripts/sanitize_case.py $c > gpurun_out/sanitize/${tool}_${c}.txt 2>&1
