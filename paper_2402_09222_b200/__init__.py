@@ -109,6 +109,21 @@ class Problem:
         return out, ck
 
 
+def div_check(a, b, device: int = 0):
+    """The event kernels' branch-free fp64 divisions on the device (parity
+    hook): (q_fast, fast_ok, q_frac, q_ieee) per pair (a[i], b[i])."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    n = len(a)
+    if len(b) != n:
+        raise ValueError("a and b differ in length")
+    qf, qr, qi = np.empty(n), np.empty(n), np.empty(n)
+    ok = np.empty(n, np.uint8)
+    _check(_lib.omcg_div_check(device, n, a.ctypes.data, b.ctypes.data, qf.ctypes.data, ok.ctypes.data,
+                               qr.ctypes.data, qi.ctypes.data))
+    return qf, ok.astype(bool), qr, qi
+
+
 @dataclass
 class RunOutput:
     result: RunResult

@@ -23,7 +23,7 @@ MAX_BATCHES = 512
 EXPORTS = (
     "omcg_version", "omcg_last_error", "omcg_problem_create", "omcg_problem_free",
     "omcg_problem_get_info", "omcg_library_checksum", "omcg_hash_build", "omcg_xs_lookup",
-    "omcg_xs_lookup_queue",
+    "omcg_xs_lookup_queue", "omcg_div_check",
     "omcg_run_config_default", "omcg_run", "omcg_queue_trace", "omcg_nccl_unique_id",
     "omcg_device_count", "omcg_bank_exchange_plan", "omcg_energy_counter_mj",
     "omcg_energy_mark", "omcg_energy_since_mark_j", "omcg_release_devices",
@@ -94,6 +94,7 @@ def load() -> C.CDLL:
     lib.omcg_xs_lookup.argtypes = [P, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.omcg_xs_lookup_queue.argtypes = [P, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
                                          C.c_void_p, C.c_void_p]
+    lib.omcg_div_check.argtypes = [C.c_int, C.c_int64] + [C.c_void_p] * 6
     lib.omcg_run_config_default.argtypes = [C.POINTER(RunConfig)]
     lib.omcg_run_config_default.restype = None
     lib.omcg_run.argtypes = [P, C.POINTER(RunConfig), C.POINTER(RunResult), C.c_void_p, C.c_void_p]

@@ -102,6 +102,16 @@ OMCG_API int omcg_hash_build(const omcg_problem* p, int n_bins, int device, uint
     });
 }
 
+OMCG_API int omcg_div_check(int device, int64_t n, const double* a, const double* b, double* q_fast,
+                            uint8_t* fast_ok, double* q_frac, double* q_ieee) {
+    return wrap([&] {
+        if (n < 0) throw std::invalid_argument("n < 0");
+        if (n == 0) return;
+        if (!a || !b || !q_fast || !fast_ok || !q_frac || !q_ieee) throw std::invalid_argument("null argument");
+        omcg::device_div_check(device, n, a, b, q_fast, fast_ok, q_frac, q_ieee);
+    });
+}
+
 OMCG_API int omcg_xs_lookup(const omcg_problem* p, int n_bins, int device, int64_t n, const int32_t* mat,
                             const double* E, double* out) {
     return wrap([&] {

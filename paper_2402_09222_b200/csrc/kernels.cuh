@@ -88,6 +88,8 @@ long long launch_counter();
 
 // library / hash
 void launch_hash_build(const DevLib& lib, int32_t* hash, cudaStream_t s);
+void launch_div_check(int64_t n, const double* a, const double* b, double* q_fast, uint8_t* ok, double* q_frac,
+                      double* q_ieee, cudaStream_t s);
 void launch_xs_pairs(const DevLib& lib, int64_t n, const int32_t* mat, const double* E, double* out,
                      cudaStream_t s);
 

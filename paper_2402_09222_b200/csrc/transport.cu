@@ -1660,6 +1660,31 @@ uint64_t device_hash_build(const Problem& p, int n_bins, int device, int32_t* ha
     return h;
 }
 
+void device_div_check(int device, int64_t n, const double* a, const double* b, double* q_fast, uint8_t* ok,
+                      double* q_frac, double* q_ieee) {
+    CK(cudaSetDevice(device));
+    cudaStream_t s;
+    CK(cudaStreamCreate(&s));
+    {
+        DevArena ar;
+        ar.device = device;
+        double* da = ar.alloc<double>(n);
+        double* db = ar.alloc<double>(n);
+        double* dq = ar.alloc<double>(3 * n);
+        uint8_t* dok = ar.alloc<uint8_t>(n);
+        CK(cudaMemcpyAsync(da, a, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        launch_div_check(n, da, db, dq, dok, dq + n, dq + 2 * n, s);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(q_fast, dq, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(q_frac, dq + n, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(q_ieee, dq + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ok, dok, n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    cudaStreamDestroy(s);
+}
+
 void device_xs_lookup(const Problem& p, int n_bins, int device, int64_t n, const int32_t* mat, const double* E,
                       double* out) {
     CK(cudaSetDevice(device));

@@ -23,6 +23,8 @@ void run_transport(const Problem& p, const omcg_run_config& cfg, omcg_run_result
                    omcg_record* records);
 
 uint64_t device_hash_build(const Problem& p, int n_bins, int device, int32_t* hash_out);
+void device_div_check(int device, int64_t n, const double* a, const double* b, double* q_fast, uint8_t* ok,
+                      double* q_frac, double* q_ieee);
 void device_xs_lookup(const Problem& p, int n_bins, int device, int64_t n, const int32_t* mat, const double* E,
                       double* out);
 void device_xs_lookup_queue(const Problem& p, int n_bins, int device, int64_t n, const int32_t* mat, const double* E,

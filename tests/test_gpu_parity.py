@@ -42,6 +42,49 @@ def test_macro_xs_bit_exact(kind, bins):
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
 
 
+def test_branch_free_division_matches_ieee():
+    """div_chk (the compiler's fast path for a / b without its slow-path
+    branch, used by the flight, collision and lookup arithmetic): wherever it
+    reports the fast path valid the quotient equals the device's '/' bit for
+    bit, and the device's '/' equals the host's IEEE division. div_frac (the
+    interpolation fraction, no fallback) equals '/' on its whole domain
+    0 <= a < b <= 2e7, including a = 0 (E on a grid point)."""
+    rng = np.random.default_rng(11)
+    n = 2_000_000
+    # arbitrary bit patterns: zeros, subnormals, huge, inf and NaN included
+    bits = rng.integers(0, 2**63, (2, n), dtype=np.uint64) | (rng.integers(0, 2, (2, n), dtype=np.uint64) << 63)
+    a, b = bits.view(np.float64)
+    # the transport's ranges: distances / direction cosines, energies, sums of squares
+    m = n // 4
+    a[:m] = rng.uniform(-30.0, 30.0, m)
+    b[:m] = rng.uniform(-1.0, 1.0, m) * np.exp(rng.uniform(-40, 0, m))
+    a[m:2 * m] = np.exp(rng.uniform(np.log(1e-5), np.log(2e7), m))
+    b[m:2 * m] = np.exp(rng.uniform(np.log(1e-5), np.log(2e7), m))
+    specials = np.array([0.0, -0.0, 1.0, -1.0, 5e-324, 2.2250738585072014e-308, 1e-300, 1e300, 1.7976931348623157e308,
+                         np.inf, -np.inf, np.nan, 1e-5, 2e7], np.float64)
+    k = len(specials)
+    a[2 * m:2 * m + k * k] = np.repeat(specials, k)
+    b[2 * m:2 * m + k * k] = np.tile(specials, k)
+    qf, ok, _, qi = P.div_check(a, b)
+    with np.errstate(all="ignore"):
+        host = a / b
+    same = lambda x, y: (x.view(np.uint64) == y.view(np.uint64)) | (np.isnan(x) & np.isnan(y))
+    assert same(qi, host).all()
+    assert same(qf[ok], qi[ok]).all()
+    assert ok[:2 * m].mean() > 0.999  # the fallback stays rare on the transport's ranges
+    # div_frac on interpolation fractions: E_lo <= E < E_hi on the library grid
+    lo = np.exp(rng.uniform(np.log(1e-5), np.log(2e7), n))
+    hi = np.minimum(lo * np.exp(rng.uniform(1e-15, 0.5, n)), 2e7)
+    hi = np.where(hi > lo, hi, np.nextafter(lo, np.inf))
+    E = lo + (hi - lo) * rng.uniform(0.0, 1.0, n)
+    E = np.where(E < hi, E, lo)
+    E[: n // 8] = lo[: n // 8]  # on a grid point: numerator exactly 0
+    num, den = E - lo, hi - lo
+    _, _, qr, qi = P.div_check(num, den)
+    assert same(qr, qi).all()
+    assert same(qi, num / den).all()
+
+
 @pytest.mark.parametrize("bins", [100, 4000])
 @pytest.mark.parametrize("sort", [None, 20000])
 @pytest.mark.parametrize("mix", ["fuel", "mixed"])
