@@ -194,11 +194,13 @@ OMCG_API int omcg_xs_lookup(const omcg_problem* p, int n_bins, int device, int64
 OMCG_API int omcg_xs_lookup_queue(const omcg_problem* p, int n_bins, int device, int64_t n, const int32_t* mat,
                                   const double* E, int64_t sort_threshold, double* out, double* ckpt_out);
 
-/* Parity hook for the event kernels' branch-free fp64 divisions (DESIGN.md
- * §4.2): per pair on the device, q_fast / fast_ok = the checked fast path
- * (div_chk) and its flag, q_frac = the interpolation-fraction form
- * (div_frac), q_ieee = a / b. Contract: fast_ok => q_fast == q_ieee bit for
- * bit; q_frac == q_ieee on the interpolation domain (0 <= a < b <= 2e7).
+/* Parity hook for the event kernels' branch-free fp64 divisions and square
+ * roots: per pair on the device, q_fast[i] / fast_ok[i] = the
+ * checked fast path a / b (div_chk) and its flag, q_frac[i] = the no-fallback
+ * form (div_frac), q_ieee[i] = a / b; q_fast[n + i] / fast_ok[n + i] /
+ * q_ieee[n + i] the same for sqrt(a) (sqrt_chk). q_fast, fast_ok and q_ieee
+ * hold 2n entries, q_frac n. Contract: fast_ok => q_fast == q_ieee bit for
+ * bit; q_frac == q_ieee on its domains (interpolation fractions, det_log).
  * No reference counterpart (test infrastructure, like omcg_xs_lookup). */
 OMCG_API int omcg_div_check(int device, int64_t n, const double* a, const double* b, double* q_fast,
                             uint8_t* fast_ok, double* q_frac, double* q_ieee);

@@ -110,18 +110,20 @@ class Problem:
 
 
 def div_check(a, b, device: int = 0):
-    """The event kernels' branch-free fp64 divisions on the device (parity
-    hook): (q_fast, fast_ok, q_frac, q_ieee) per pair (a[i], b[i])."""
+    """The event kernels' branch-free fp64 divisions and square roots on the
+    device (parity hook): (q_fast, fast_ok, q_frac, q_ieee, s_fast, s_ok,
+    s_ieee) — a[i] / b[i] three ways, sqrt(a[i]) two ways."""
     a = np.ascontiguousarray(a, np.float64)
     b = np.ascontiguousarray(b, np.float64)
     n = len(a)
     if len(b) != n:
         raise ValueError("a and b differ in length")
-    qf, qr, qi = np.empty(n), np.empty(n), np.empty(n)
-    ok = np.empty(n, np.uint8)
+    qf, qr, qi = np.empty(2 * n), np.empty(n), np.empty(2 * n)
+    ok = np.empty(2 * n, np.uint8)
     _check(_lib.omcg_div_check(device, n, a.ctypes.data, b.ctypes.data, qf.ctypes.data, ok.ctypes.data,
                                qr.ctypes.data, qi.ctypes.data))
-    return qf, ok.astype(bool), qr, qi
+    ok = ok.astype(bool)
+    return qf[:n], ok[:n], qr, qi[:n], qf[n:], ok[n:], qi[n:]
 
 
 @dataclass

@@ -1670,16 +1670,16 @@ void device_div_check(int device, int64_t n, const double* a, const double* b, d
         ar.device = device;
         double* da = ar.alloc<double>(n);
         double* db = ar.alloc<double>(n);
-        double* dq = ar.alloc<double>(3 * n);
-        uint8_t* dok = ar.alloc<uint8_t>(n);
+        double* dq = ar.alloc<double>(5 * n);  // fast (div, sqrt), frac, ieee (div, sqrt)
+        uint8_t* dok = ar.alloc<uint8_t>(2 * n);
         CK(cudaMemcpyAsync(da, a, sizeof(double) * n, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-        launch_div_check(n, da, db, dq, dok, dq + n, dq + 2 * n, s);
+        launch_div_check(n, da, db, dq, dok, dq + 2 * n, dq + 3 * n, s);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(q_fast, dq, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(q_frac, dq + n, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(q_ieee, dq + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(ok, dok, n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(q_fast, dq, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(q_frac, dq + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(q_ieee, dq + 3 * n, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ok, dok, 2 * n, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     }
     cudaStreamDestroy(s);

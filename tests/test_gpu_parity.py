@@ -47,8 +47,8 @@ def test_branch_free_division_matches_ieee():
     branch, used by the flight, collision and lookup arithmetic): wherever it
     reports the fast path valid the quotient equals the device's '/' bit for
     bit, and the device's '/' equals the host's IEEE division. div_frac (the
-    interpolation fraction, no fallback) equals '/' on its whole domain
-    0 <= a < b <= 2e7, including a = 0 (E on a grid point)."""
+    interpolation fraction and det_log's mantissa quotient, no fallback)
+    equals '/' on both domains, including a = 0 (E on a grid point, m = 1)."""
     rng = np.random.default_rng(11)
     n = 2_000_000
     # arbitrary bit patterns: zeros, subnormals, huge, inf and NaN included
@@ -65,13 +65,17 @@ def test_branch_free_division_matches_ieee():
     k = len(specials)
     a[2 * m:2 * m + k * k] = np.repeat(specials, k)
     b[2 * m:2 * m + k * k] = np.tile(specials, k)
-    qf, ok, _, qi = P.div_check(a, b)
+    qf, ok, _, qi, sf, sok, si = P.div_check(a, b)
     with np.errstate(all="ignore"):
-        host = a / b
+        host, hsqrt = a / b, np.sqrt(a)
     same = lambda x, y: (x.view(np.uint64) == y.view(np.uint64)) | (np.isnan(x) & np.isnan(y))
     assert same(qi, host).all()
     assert same(qf[ok], qi[ok]).all()
     assert ok[:2 * m].mean() > 0.999  # the fallback stays rare on the transport's ranges
+    # sqrt_chk: the same contract for the square roots
+    assert same(si, hsqrt).all()
+    assert same(sf[sok], si[sok]).all()
+    assert sok[m:2 * m].all() and sok.mean() > 0.45
     # div_frac on interpolation fractions: E_lo <= E < E_hi on the library grid
     lo = np.exp(rng.uniform(np.log(1e-5), np.log(2e7), n))
     hi = np.minimum(lo * np.exp(rng.uniform(1e-15, 0.5, n)), 2e7)
@@ -80,9 +84,13 @@ def test_branch_free_division_matches_ieee():
     E = np.where(E < hi, E, lo)
     E[: n // 8] = lo[: n // 8]  # on a grid point: numerator exactly 0
     num, den = E - lo, hi - lo
-    _, _, qr, qi = P.div_check(num, den)
+    _, _, qr, qi, _, _, _ = P.div_check(num, den)
     assert same(qr, qi).all()
     assert same(qi, num / den).all()
+    # det_log's (m - 1) / (m + 1) on its reduced mantissa m in [sqrt(2)/2, sqrt(2)], m = 1 included
+    m = np.concatenate([rng.uniform(np.sqrt(0.5), np.sqrt(2.0), n), [1.0, np.nextafter(1.0, 0), np.nextafter(1.0, 2)]])
+    _, _, qr, qi, _, _, _ = P.div_check(m - 1.0, m + 1.0)
+    assert same(qr, qi).all()
 
 
 @pytest.mark.parametrize("bins", [100, 4000])
