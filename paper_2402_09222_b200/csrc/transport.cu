@@ -264,6 +264,8 @@ struct GpuProblem {
         lib.n_dens = (int)host_dens.size();
         launch_hash_build(lib, d_hash, s);
         CK(cudaGetLastError());
+        if ((int64_t)p.geo.nx * p.geo.ny > (1 << 20))  // cell_xy's exact range (kernels.cu)
+            throw std::invalid_argument("more than 2^20 lattice cells");
         geo = p.geo;
         geo.pin_map = d_pin;
     }
