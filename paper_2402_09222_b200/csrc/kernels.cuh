@@ -97,6 +97,7 @@ void launch_xs_pairs(const DevLib& lib, int64_t n, const int32_t* mat, const dou
 void launch_lookup_setup(const Ctx& c, int n, const int32_t* mat, const double* E, int32_t* q, cudaStream_t s);
 
 // event kernels; q == nullptr selects the queueless variant over all cap slots
+void launch_publish(const unsigned* count, unsigned* host, unsigned seq, cudaStream_t s);
 void launch_init(const Ctx& c, uint64_t head, int n, int64_t first_local, const Site* src, cudaStream_t s);
 // warp-per-history tail over the `live` remaining histories, listed into
 // `list` first (ctrl[3] must be zero)

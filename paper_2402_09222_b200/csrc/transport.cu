@@ -8,6 +8,7 @@
 // mode (P0 = "openmc-queueless") sweeps all event kernels over every slot
 // (PAPER.md:219-221). Between batches the rank reduces int64 tallies and
 // k-eff accumulators with NCCL and redistributes the canonical fission bank.
+#include <atomic>
 #include <dlfcn.h>
 #include <nccl.h>
 #include <nvtx3/nvToolsExt.h>
@@ -285,6 +286,8 @@ struct SubBank {
     unsigned* cursor = nullptr;
     unsigned* bsum = nullptr;
     unsigned* h_counts = nullptr;  // pinned: live queue lengths [0..4], then dead tail (as 2 words)
+    unsigned* d_h_counts = nullptr;  // its device alias (k_publish writes words 0-7, then the sequence word 8)
+    unsigned pub_seq = 0;
     uint64_t dead_head = 0;        // ring head (host side; only the refill consumes)
     ull* ctrl = nullptr;           // [0] ticket [1] alive [2] errors
     ull* h_ctrl = nullptr;         // pinned
@@ -462,6 +465,8 @@ void setup_rank(Rank& R, const Problem& p, const omcg_run_config& cfg) {
         S.trace_chk = A.alloc<ull>(1);
         CK(cudaMemsetAsync(S.ctrl, 0, sizeof(ull) * 8, S.stream));
         S.h_counts = static_cast<unsigned*>(pinned().get());  // 8 words
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S.d_h_counts), S.h_counts, 0));
+        S.h_counts[8] = S.pub_seq = 0;
         S.h_ctrl = static_cast<ull*>(pinned().get());         // 4 words
         S.h_trace_chk = static_cast<ull*>(pinned().get());
         S.sched = A.alloc<DevSched>(1);
@@ -684,6 +689,22 @@ void run_device_loop(Rank& R, SubBank& S, Ctx& c, const omcg_run_config& cfg, bo
     }
 }
 
+// Spin until k_publish's sequence word arrives; poll the stream now and then so
+// a failed kernel (which never publishes) surfaces as an error instead of a hang.
+void wait_published(SubBank& S) {
+    volatile unsigned* h = S.h_counts;
+    for (unsigned spins = 1;; ++spins) {
+        if (h[8] == S.pub_seq) break;
+        if ((spins & 1023u) == 0) {
+            const cudaError_t e = cudaStreamQuery(S.stream);
+            if (e != cudaSuccess && e != cudaErrorNotReady) CK(e);
+            if (e == cudaSuccess && h[8] != S.pub_seq)
+                throw std::logic_error("queue-length read-back: stream idle without the published counts");
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+}
+
 void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_config& cfg, bool prof,
                 int fuel_nuc) {
     int64_t next = S.lo;
@@ -697,7 +718,15 @@ void run_queued(Rank& R, SubBank& S, Ctx c, const Site* src, const omcg_run_conf
     bool known = false, check_prediction = false;
     unsigned predicted[8];
     for (;;) {
-        if (!known) {
+        if (!known && !pending_trace) {
+            // k_publish writes the counts to page-locked memory; spin on its sequence word
+            launch_publish(S.qs.count, S.d_h_counts, ++S.pub_seq, S.stream);
+            wait_published(S);
+            S.n_done = S.n_pending;
+            if (check_prediction && std::memcmp(predicted, S.h_counts, sizeof predicted) != 0)
+                throw std::logic_error("queue-length prediction after a fuel calculate_xs launch was wrong");
+            check_prediction = false;
+        } else if (!known) {
             CK(cudaMemcpyAsync(S.h_counts, S.qs.count, sizeof(unsigned) * 8, cudaMemcpyDeviceToHost, S.stream));
             if (pending_trace)
                 CK(cudaMemcpyAsync(S.h_trace_chk, S.trace_chk, sizeof(ull), cudaMemcpyDeviceToHost, S.stream));
